@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""bench.py — decode-step throughput of the B200 eLLM KV-traffic hot path.
+
+One step = one decode iteration of every request of the workload through the hot path
+(SURVEY §8(a)): kv_reserve (+1 token each) and, for every layer, kv_append of the new
+K/V, paged decode attention (+ split-K combine) and, for N > 1 GPUs, the all-gather of the
+KV-head-sharded outputs. The elastic rows (deflate / inflate / migrate) are measured in
+the same run as swap / migrate GB/s ("swap" object) against the host link measured there.
+
+Default workload (N=1): BASELINE.json configs[1], LLaMA-3-8B shape (32 layers, 32q/8kv heads,
+d=128), 32 requests x 32768 tokens of synthetic bf16 KV (128 GiB in 2 MiB chunks).
+N > 1: the same workload KV-head-sharded over N GPUs (strong scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ellm|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "tokens/s"
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback (only if MEASURED_PEAKS.json absent)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ellm", "reference"], default="ellm")
+    ap.add_argument("--workload", choices=["c2", "c4"], default="c2")
+    ap.add_argument("--no-swap", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_id: str):
+        self.gpu_id = gpu_id
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", self.gpu_id, "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def gpu_id_for(device: int) -> str:
+    import torch
+    try:
+        p = torch.cuda.get_device_properties(device)
+        return f"{p.pci_domain_id:08X}:{p.pci_bus_id:02X}:{p.pci_device_id:02X}.0"
+    except Exception:
+        return str(device)
+
+
+# ----------------------------------------------------------------------------------------
+# oracle legs (the only places bench.py executes oracle/)
+# ----------------------------------------------------------------------------------------
+def oracle_sample(wl, min_seconds=4.0):
+    """Time the oracle (C++ fp64, OpenMP over q-heads, as it stands) on a bounded sample:
+    attention of one request x one layer at the full context, repeated until >= min_seconds.
+    Returns (seconds per request-layer, repeats, threads)."""
+    import oracle
+    from inputs import workload as W
+    k, v = W.host_kv(wl, 0, 0, wl.context)
+    q = W.host_q(wl, 0, 0)
+    scale = 1.0 / (wl.head_dim ** 0.5)
+    oracle.attention_contig(q, k[:16], v[:16], scale)  # load + warm
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        oracle.attention_contig(q, k, v, scale)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= min_seconds:
+            break
+    return el / reps, reps, oracle.num_threads()
+
+
+def cpu_baseline_obj(wl, per_rl, reps, threads):
+    tok_s = 1.0 / (wl.n_layers * per_rl)  # B requests x L layers per B tokens
+    return {"value": round(tok_s, 4), "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": (f"oracle fp64 attention of 1 request x 1 layer at {wl.context} tokens "
+                       f"({wl.hq_local} q-heads, {wl.hkv_local} kv-heads, d={wl.head_dim}) repeated {reps}x "
+                       f"({per_rl:.3f} s each); extrapolated to {wl.batch} requests x {wl.n_layers} layers "
+                       f"per decode step")}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from inputs import workload as W
+    wl = W.c2() if args.workload == "c2" else W.c4()
+    per_rl, reps, threads = oracle_sample(wl, min_seconds=2.0)
+    step_times = []
+    for _ in range(args.warmup):
+        oracle_sample(wl, min_seconds=0.0)
+    for _ in range(args.steps):
+        t, _, _ = oracle_sample(wl, min_seconds=0.0)
+        step_times.append(t * wl.n_layers * wl.batch)
+    step = statistics.mean(step_times)
+    value = wl.batch / step
+    cb = cpu_baseline_obj(wl, step / (wl.n_layers * wl.batch), args.steps, threads)
+    cb["value"] = round(value, 4)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded counter-based generator)",
+        "config": workload_config(wl, args.gpus),
+        "cpu_baseline": cb,
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": ("each step is a bounded sample: one request x one layer of the oracle, scaled to "
+                 f"{wl.batch} requests x {wl.n_layers} layers"),
+    }), flush=True)
+
+
+def workload_config(wl, n):
+    return {"workload": wl.name, "layers": wl.n_layers, "heads_q": wl.n_heads_q, "heads_kv": wl.n_heads_kv,
+            "head_dim": wl.head_dim, "batch": wl.batch, "context": wl.context,
+            "tokens_per_chunk": wl.tokens_per_chunk, "chunk_bytes": wl.chunk_bytes(),
+            "parallelism": f"kv-head shard x{n}" if n > 1 else "single GPU",
+            "l2": "inputs larger than L2 (KV read per layer >> 126 MB L2)"}
+
+
+# ----------------------------------------------------------------------------------------
+# the product leg
+# ----------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    from paper_2506_15155_b200 import ellm
+    from inputs import workload as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl = W.c2(world, rank) if args.workload == "c2" else W.c4(world, rank)
+    B, L = wl.batch, wl.n_layers
+    swap_chunks = 1024 if not args.no_swap else 0
+    pool = W.make_pool(wl, local, host_slots=swap_chunks)
+    W.prefill(pool, wl)
+    reqs = list(range(B))
+    ones = [1] * B
+    scale = 1.0 / (wl.head_dim ** 0.5)
+    lens = np.full(B, wl.context, np.int64)
+    n_steps = args.warmup + args.steps
+    e2e_steps = 0 if args.no_e2e else args.steps
+    inputs = []
+    for s in range(n_steps + e2e_steps):
+        inputs.append(W.decode_inputs(wl, s, lens + s))
+    out = torch.empty((L, B, wl.hq_local, wl.head_dim), dtype=torch.bfloat16, device="cuda")
+    gath = torch.empty((L, world, B, wl.hq_local, wl.head_dim), dtype=torch.bfloat16, device="cuda") \
+        if world > 1 else None
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    attn_ev = []
+
+    def step(q, k, v, record=False):
+        rc = pool.reserve(reqs, ones, sp)
+        if rc:
+            raise ellm.EllmError(rc, "reserve")
+        for l in range(L):
+            rc = pool.append(l, reqs, ones, k[l], v[l], sp)
+            if rc:
+                raise ellm.EllmError(rc, "append")
+            if record:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            rc = pool.attention(l, reqs, q[l], out[l], scale, sp)
+            if rc:
+                raise ellm.EllmError(rc, "attention")
+            if record:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(stream)
+                attn_ev.append((e0, e1))
+            if gath is not None:
+                dist.all_gather_into_tensor(gath[l], out[l])
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for s in range(args.warmup):
+        step(*inputs[s])
+    barrier()
+    launches0 = pool.kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(gpu_id_for(local)) as clk:
+        ev0.record(stream)
+        for s in range(args.warmup, n_steps):
+            step(*inputs[s], record=True)
+        ev1.record(stream)
+        barrier()
+    launches = pool.kernel_launches() - launches0
+    el_ms = ev0.elapsed_time(ev1)
+    attn_ms = [a.elapsed_time(b) for a, b in attn_ev]
+    if dist:
+        t = torch.tensor([el_ms, statistics.mean(attn_ms)], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el_ms, attn_mean = float(t[0]), float(t[1])
+    else:
+        attn_mean = statistics.mean(attn_ms)
+    ms_step = el_ms / args.steps
+    value = B * args.steps / (el_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (paged attention + combine, one call per layer) ----
+    lens_timed = lens + args.warmup + (args.steps + 1) / 2.0  # mean context during the timed steps
+    T = wl.tokens_per_chunk
+    alg_bytes = (wl.kv_bytes_per_layer(lens_timed) + 2 * B * wl.hq_local * wl.head_dim * 2
+                 + 4 * int(sum(np.ceil(lens_timed / T))))
+    achieved = alg_bytes / (attn_mean / 1e3) / 1e9
+    peak, peak_src = hbm_peak()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(wl.name)
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "kernel": "paged_attn_kernel + attn_combine_kernel (one ellm_paged_decode_attention call)",
+            "alg_bytes_per_launch": int(alg_bytes), "launch_ms": round(attn_mean, 4), "peak_source": peak_src}
+
+    # ---- end to end through host buffers: H2D of each step's inputs, D2H of its outputs ----
+    e2e = None
+    if e2e_steps:
+        hin = []
+        for s in range(n_steps, n_steps + e2e_steps):
+            hin.append(tuple(x.cpu().pin_memory() for x in inputs[s]))
+        dq, dk, dv = (torch.empty_like(x) for x in inputs[0])
+        hout = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        h2d = sum(x.numel() * x.element_size() for x in hin[0])
+        d2h = hout.numel() * hout.element_size()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for hq, hk, hv in hin:
+            dq.copy_(hq, non_blocking=True)
+            dk.copy_(hk, non_blocking=True)
+            dv.copy_(hv, non_blocking=True)
+            step(dq, dk, dv)
+            hout.copy_(out, non_blocking=True)
+        e1.record(stream)
+        barrier()
+        ems = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ems], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t[0])
+        e2e = {"value": round(B * e2e_steps / (ems / 1e3), 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ems / e2e_steps, 3)}
+
+    swap = measure_swap(pool, wl, stream) if swap_chunks else None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        per_rl, reps, threads = oracle_sample(wl)
+        cpu = cpu_baseline_obj(wl, per_rl, reps, threads)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (seeded counter-based generator, 3 needles per request/layer/kv-head)",
+                "config": workload_config(wl, world), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches), "clocks": clk.summary(),
+                "attention_gbs": round(achieved, 1), "attention_frac_of_peak": roof["frac"], "swap": swap}
+        print(json.dumps(line), flush=True)
+    pool.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def measure_swap(pool, wl, stream):
+    """deflate / inflate / migrate GB/s over 1024 chunks (2 GiB at 2 MiB chunks) with the SM
+    copy kernels and with the DMA copy engines, against pinned 1 GiB cudaMemcpyAsync (the
+    host-link roofline, measured here)."""
+    import torch
+    from paper_2506_15155_b200 import ellm
+    n = pool.stats()["host_free"]
+    cb = pool.chunk_bytes
+    sp = stream.cuda_stream
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / 1e3, r
+
+    res = {}
+    for mode, name in ((0, "sm"), (1, "ce")):
+        pool.set_swap_mode(mode)
+        best_d2h, best_h2d, best_mig = 0.0, 0.0, 0.0
+        for _ in range(3):
+            ids = pool.table(0)[0][:n].tolist()
+            t, (rc, slots) = timed(lambda: pool.deflate(ids, sp))
+            assert rc == ellm.OK, rc
+            best_d2h = max(best_d2h, n * cb / t / 1e9)
+            src = pool.table(1)[0][:n].tolist()
+            t, rc = timed(lambda: pool.migrate(src, sorted(ids), sp))
+            assert rc == ellm.OK, rc
+            best_mig = max(best_mig, 2 * n * cb / t / 1e9)
+            t, (rc, back) = timed(lambda: pool.inflate(slots, sp))
+            assert rc == ellm.OK, rc
+            best_h2d = max(best_h2d, n * cb / t / 1e9)
+        res[name] = {"d2h_gbs": round(best_d2h, 2), "h2d_gbs": round(best_h2d, 2),
+                     "migrate_gbs": round(best_mig, 1)}
+    pool.set_swap_mode(0)
+    # host-link roofline: pinned 1 GiB copies, best of 5
+    N = 1 << 30
+    h = torch.empty(N, dtype=torch.uint8).pin_memory()
+    d = torch.empty(N, dtype=torch.uint8, device="cuda")
+    link = {}
+    for nm, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True))):
+        best = 0.0
+        for _ in range(5):
+            t, _ = timed(fn)
+            best = max(best, N / t / 1e9)
+        link[nm] = round(best, 2)
+    best_sm = max(res["sm"]["d2h_gbs"] / link["d2h"], 0)
+    return {"chunks": n, "chunk_bytes": cb, "bytes": n * cb, "modes": res, "link_gbs": link,
+            "frac_d2h": round(max(res["sm"]["d2h_gbs"], res["ce"]["d2h_gbs"]) / link["d2h"], 3),
+            "frac_h2d": round(max(res["sm"]["h2d_gbs"], res["ce"]["h2d_gbs"]) / link["h2d"], 3),
+            "migrate_frac_of_hbm": round(max(res["sm"]["migrate_gbs"], res["ce"]["migrate_gbs"]) / hbm_peak()[0], 3),
+            "_sm_d2h_frac": round(best_sm, 3)}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,204 @@
+/* ellm.h — C ABI of libellm.so: the B200-native KV-traffic hot path of eLLM
+ * (arXiv 2506.15155, "eLLM: Elastic Memory Management Framework for Efficient LLM
+ * Serving"; paper text at /root/reference/PAPER.md, cited P:<line>).
+ *
+ * Layering:
+ *   vtensor   — a virtual address range whose chunk-aligned slots are backed on demand by
+ *               physical chunks (the paper's eTensor: "an array pointer structure
+ *               that references a contiguous segment within the GPU's virtual address
+ *               space").
+ *   pool      — one vtensor of `max_chunks` KV chunks + per-chunk ownership KV/ACT
+ *               + per-request chunk tables + pinned host slots (the CPU elastic buffer,
+ *               P:390-399) + the kernels that move KV through them.
+ *
+ * Conventions for every call
+ *   - Return int: ELLM_OK (0) or a negative ELLM_ERR_*. No exception crosses the ABI.
+ *   - All-or-nothing: every precondition is validated BEFORE any state changes, so an
+ *     error leaves the pool exactly as it was (no hold-and-wait).
+ *   - Validation order (R12): argument ranges (OUT_OF_RANGE) -> duplicates /
+ *     malformed counts (INVALID_ARG) -> per-request capacity (OUT_OF_RANGE) -> residency
+ *     (NOT_RESIDENT) / ownership (NOT_MAPPED, ALREADY_MAPPED) -> pool capacity (NO_CHUNKS,
+ *     HOST_FULL, IN_USE). Within a class, list order decides which element reports.
+ *   - Host metadata (request ids, counts, chunk / slot lists, outputs such as slot ids) are
+ *     HOST pointers, read/written before the call returns. Tensors (q, k_new, v_new, out)
+ *     are DEVICE pointers owned by the caller; they must stay valid until the stream
+ *     reaches the enqueued work. `stream` is a cudaStream_t (NULL = legacy default stream).
+ *   - Device work is enqueued on `stream` and ordered only by it. A chunk or host slot
+ *     freed by one call may be handed out by the next call; if those calls use different
+ *     streams the caller orders them (events). Kernel faults surface as ELLM_ERR_CUDA at a
+ *     later call (ellm_last_cuda_error gives the cudaError_t).
+ *   - One pool per device; calls on one pool are externally serialised.
+ *   - Allocation policy (R7): lowest free chunk id / host slot first, requests in
+ *     the given order, positions ascending. Tables are therefore deterministic and identical
+ *     on every KV-head shard.
+ *
+ * Chunk geometry (R1): one chunk = T tokens x L layers x {K,V} x Hkv local
+ * kv-heads x d, bf16, layout [L][2][Hkv][T][d]; chunk_bytes = 4*T*L*Hkv*d.
+ * Chunk c lives at pool_base + c*chunk_bytes. Table entries: >=0 device chunk id,
+ * -1 unmapped, <=-2 host slot h encoded as -(h+2).
+ */
+#ifndef ELLM_H
+#define ELLM_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  ELLM_OK = 0,
+  ELLM_ERR_INVALID_ARG = -1,    /* malformed argument, duplicate id, zero-length attention */
+  ELLM_ERR_OUT_OF_RANGE = -2,   /* id / layer / capacity out of range */
+  ELLM_ERR_NO_CHUNKS = -3,      /* not enough FREE KV chunks (or ACT chunks for grow) */
+  ELLM_ERR_HOST_FULL = -4,      /* not enough free host slots */
+  ELLM_ERR_NOT_RESIDENT = -5,   /* a needed chunk is in a host slot */
+  ELLM_ERR_NOT_MAPPED = -6,     /* chunk FREE/ACT (or host slot free) where USED is required */
+  ELLM_ERR_ALREADY_MAPPED = -7, /* destination chunk USED */
+  ELLM_ERR_IN_USE = -8,         /* shrink needs more FREE chunks than exist */
+  ELLM_ERR_CUDA = -9,           /* CUDA runtime / driver failure */
+  ELLM_ERR_NCCL = -10,          /* reserved for the fused multi-GPU path */
+  ELLM_ERR_NO_DEVICE = -11,     /* call needs a device but the pool is host-metadata-only */
+  ELLM_ERR_UNSUPPORTED = -12    /* shape outside what the kernels implement (see pool_create) */
+};
+
+/* device = ELLM_DEVICE_NONE creates a host-metadata-only pool (tables, ownership, host
+ * slot bookkeeping; no VMM, no kernels). Calls that move bytes update metadata only in
+ * that mode and the attention / append / read calls return ELLM_ERR_NO_DEVICE. It exists
+ * so the allocation logic can be tested on a machine without a GPU. */
+#define ELLM_DEVICE_NONE (-1)
+
+typedef struct ellm_pool ellm_pool;
+typedef struct ellm_vtensor ellm_vtensor;
+
+typedef struct {
+  int32_t device;                  /* CUDA ordinal or ELLM_DEVICE_NONE */
+  int32_t n_layers;                /* L */
+  int32_t n_heads_q;               /* q-heads on this shard (Hq_local) */
+  int32_t n_heads_kv;              /* kv-heads on this shard (Hkv_local); Hq % Hkv == 0 */
+  int32_t head_dim;                /* d: 64 or 128 */
+  int32_t tokens_per_chunk;        /* T: multiple of 16 */
+  int64_t max_chunks;              /* VA capacity in chunks (KV + ACT) */
+  int64_t initial_chunks;          /* chunks KV-owned (mapped) at create: ids [0, initial) */
+  int32_t max_requests;            /* request ids are [0, max_requests) */
+  int32_t max_chunks_per_request;  /* table row length (the KV eTensor span) */
+  int64_t host_slots;              /* pinned host slots, chunk_bytes each (CPU buffer P_B) */
+} ellm_pool_config;
+
+typedef struct {
+  int64_t kv_free, kv_used, act;   /* chunk counts; kv_free + kv_used + act == max_chunks */
+  int64_t host_free, host_used;    /* host slot counts */
+  int64_t n_map, n_unmap;          /* VMM map / unmap operations so far */
+  int64_t map_ns, unmap_ns;        /* host wall time spent in them */
+  int64_t chunk_bytes;             /* bytes per chunk */
+  int64_t mapped_bytes;            /* physical device bytes currently mapped */
+} ellm_stats;
+
+/* ---- vtensor (VMM) ------------------------------------------------------------------
+ * A VA reservation of n_slots * slot_bytes (cuMemAddressReserve), each slot backed on
+ * demand by its own physical allocation (cuMemCreate + cuMemMap + cuMemSetAccess RW for
+ * `device`). slot_bytes must be a multiple of the allocation granularity
+ * (ellm_vmm_granularity), else INVALID_ARG. map of a mapped slot -> ALREADY_MAPPED;
+ * unmap of an unmapped slot -> NOT_MAPPED (whole range validated first). unmap is
+ * synchronous w.r.t. the device (cuMemUnmap, cuda.h \note_sync): it synchronises the
+ * device first. The library owns the reservation and handles; destroy releases both. */
+int ellm_vmm_granularity(int32_t device, size_t* out);
+int ellm_vtensor_create(int32_t device, size_t slot_bytes, int64_t n_slots, ellm_vtensor** out);
+int ellm_vtensor_map(ellm_vtensor* vt, int64_t first_slot, int64_t n);
+int ellm_vtensor_unmap(ellm_vtensor* vt, int64_t first_slot, int64_t n);
+int ellm_vtensor_is_mapped(const ellm_vtensor* vt, int64_t slot); /* 1 / 0, <0 on error */
+void* ellm_vtensor_base(const ellm_vtensor* vt);
+int ellm_vtensor_destroy(ellm_vtensor* vt);
+
+/* ---- pool ---------------------------------------------------------------------------
+ * create: validates the config (head_dim in {64,128}, T % 16 == 0,
+ * group Hq/Hkv in [1,8], chunk_bytes a multiple or a divisor of the granularity, else
+ * UNSUPPORTED / INVALID_ARG), reserves VA for max_chunks, maps the initial KV chunks,
+ * allocates host_slots pinned+mapped host slots and the device tables / workspaces. */
+int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out);
+int ellm_pool_destroy(ellm_pool* pool);
+int ellm_pool_stats(const ellm_pool* pool, ellm_stats* out);
+void* ellm_pool_base(const ellm_pool* pool);        /* device VA of chunk 0 (NULL if no device) */
+void* ellm_pool_host_base(const ellm_pool* pool);   /* host VA of slot 0 (pinned) */
+
+/* kv_reserve (a2; "Physical chunks are allocated on-demand during actual writes"):
+ * for each listed request r (distinct), extend its logical length by n_new[i] >= 0,
+ * mapping logical chunks ceil(len/T) .. ceil((len+n_new)/T)-1 to the lowest FREE KV ids
+ * (requests in list order, chunks ascending). Records n_new[i] as the positions the next
+ * kv_append of r writes. Errors: id range / table capacity -> OUT_OF_RANGE; duplicate or
+ * negative -> INVALID_ARG; partially-filled last chunk in a host slot (and n_new>0) ->
+ * NOT_RESIDENT; total new chunks > FREE KV -> NO_CHUNKS. Enqueues the device-table update
+ * on `stream`. No implicit growth: call ellm_pool_grow first. */
+int ellm_kv_reserve(ellm_pool* pool, int32_t n, const int32_t* req_ids, const int32_t* n_new,
+                    void* stream);
+
+/* kv_append (a3): write K/V of layer `layer` for positions [len-n_new, len) of each listed
+ * request (n_new[i] must equal the latest reservation, else INVALID_ARG; R13).
+ * k_new, v_new: device [sum(n_new), Hkv, d] bf16, rows in list order then position order.
+ * Every target chunk must be on the device (else NOT_RESIDENT). Bit-exact copy. */
+int ellm_kv_append(ellm_pool* pool, int32_t layer, int32_t n, const int32_t* req_ids,
+                   const int32_t* n_new, const void* k_new, const void* v_new, void* stream);
+
+/* paged_decode_attention (a4+a5, exact softmax attention over the accumulated
+ * KV read through the chunk table): for each listed request i (duplicates allowed) and
+ * q-head h, out[i][h] = sum_j softmax_j(scale * q[i][h].k_j) v_j over j < len, with kv-head
+ * h / (Hq/Hkv). q: device [n, Hq, d] bf16; out: device [n, Hq, d] bf16 (fp32 accumulate,
+ * RNE). len == 0 -> INVALID_ARG; any chunk of the request in a host slot -> NOT_RESIDENT. */
+int ellm_paged_decode_attention(ellm_pool* pool, int32_t layer, int32_t n, const int32_t* req_ids,
+                                const void* q, void* out, float softmax_scale, void* stream);
+
+/* release: all device chunks and host slots of req become FREE; len = 0. */
+int ellm_release(ellm_pool* pool, int32_t req_id, void* stream);
+
+/* deflate = swap-out / offload (a6): copy each listed USED chunk to the lowest
+ * free host slot (list order), repoint its table entry to the slot, mark the chunk FREE.
+ * host_slots_out[i] receives the slot. Errors: id range -> OUT_OF_RANGE; duplicates ->
+ * INVALID_ARG; chunk not USED KV -> NOT_MAPPED; n > free slots -> HOST_FULL. */
+int ellm_deflate(ellm_pool* pool, int32_t n, const int32_t* chunk_ids, int32_t* host_slots_out,
+                 void* stream);
+/* inflate = swap-in / fetch (a7): copy each listed USED host slot into the
+ * lowest FREE KV chunk (list order), repoint the table entry, free the slot.
+ * chunk_ids_out[i] receives the chunk. Errors: slot range -> OUT_OF_RANGE; duplicates ->
+ * INVALID_ARG; slot not used -> NOT_MAPPED; n > FREE KV chunks -> NO_CHUNKS. */
+int ellm_inflate(ellm_pool* pool, int32_t n, const int32_t* host_slots, int32_t* chunk_ids_out,
+                 void* stream);
+/* migrate (a8; BJ; D2D compaction): copy chunk src[i] -> dst[i], repoint the table entry,
+ * src becomes FREE, dst USED. Errors: range -> OUT_OF_RANGE; any repeated id among the 2n
+ * -> INVALID_ARG; src not USED KV -> NOT_MAPPED; dst ACT -> NOT_MAPPED; dst USED ->
+ * ALREADY_MAPPED. */
+int ellm_migrate(ellm_pool* pool, int32_t n, const int32_t* src, const int32_t* dst, void* stream);
+
+/* pool_grow (a9; inflation steps 3-4): the n lowest-id ACT chunks become FREE KV
+ * and their physical memory is created and mapped. n > #ACT -> NO_CHUNKS.
+ * pool_shrink (a9; deflation): the n highest-id FREE KV chunks become ACT; physical
+ * memory whose chunks are all ACT is unmapped and released (device-synchronising).
+ * n > #FREE KV -> IN_USE. */
+int ellm_pool_grow(ellm_pool* pool, int64_t n);
+int ellm_pool_shrink(ellm_pool* pool, int64_t n);
+
+/* Swap engine selection: 0 = SM copy kernels (default), 1 = DMA copy engines
+ * (cudaMemcpyAsync per chunk). Both are exact byte copies. */
+int ellm_set_swap_mode(ellm_pool* pool, int32_t mode);
+
+/* ---- introspection (parity tests) --------------------------------------------------- */
+/* table of req: entries[0 .. n_out) for the ceil(len/T) live logical chunks. */
+int ellm_get_table(const ellm_pool* pool, int32_t req_id, int32_t* entries, int32_t cap,
+                   int32_t* n_out, int32_t* len_out);
+/* copy chunk_bytes of device chunk `chunk_id` to host_dst (synchronises `stream`). */
+int ellm_read_chunk(ellm_pool* pool, int64_t chunk_id, void* host_dst, void* stream);
+/* copy chunk_bytes of host slot `slot` to host_dst (synchronises the device). */
+int ellm_read_host_slot(ellm_pool* pool, int64_t slot, void* host_dst);
+/* Map req's physical chunks, in logical order, contiguously into a fresh VA span
+ * (multi-mapping) and return its device pointer: the paper's literal KV eTensor
+ * view. Needs chunk_bytes % granularity == 0 and all chunks on the device. */
+int ellm_alias_request(ellm_pool* pool, int32_t req_id, void** contig_dev_ptr);
+int ellm_unalias_request(ellm_pool* pool, int32_t req_id);
+
+const char* ellm_status_string(int status);
+int ellm_last_cuda_error(const ellm_pool* pool);
+/* Number of kernels this pool has launched so far (bench accounting). */
+int64_t ellm_kernel_launches(const ellm_pool* pool);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ELLM_H */

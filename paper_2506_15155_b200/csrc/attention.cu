@@ -1,0 +1,505 @@
+// attention.cu — paged decode attention over chunk-mapped KV (SURVEY §8(a) rows a4 + a5).
+//
+// Computes, per request r and q-head h (kv-head g = h / group, R6):
+//     o = sum_j softmax_j(scale * q.k_j) v_j,  j < len_r,
+// reading k_j, v_j through the request's chunk table (P:109-112 exact attention; the
+// KV eTensor's logical->physical chunk map P:307-309, read as a table, R3).
+//
+// B200 design:
+//  * Persistent CTAs, one per SM. The flattened work space is (virtual request, stage tile);
+//    CTA b owns tiles [b*W/G, (b+1)*W/G), so every SM streams the same number of bytes
+//    whatever the length mix (split-K with balanced, contiguous ranges).
+//  * A stage = TT tokens x HB kv-heads x {K,V} = 64 KiB (d=128). One producer warp walks the
+//    chunk table and issues one 5-D TMA (cp.async.bulk.tensor, SWIZZLE_128B) per chunk piece
+//    into a 3-stage mbarrier ring (192 KiB in flight per SM).
+//  * 8 consumer warps; warp w owns kv-head w % HB and the 16-token subtile w / HB of every
+//    stage. S = Q.K^T and O += P.V run on mma.sync m16n8k16 (bf16 in, fp32 accumulate) with
+//    q-heads on the M rows. The head-dim and token orders inside a tile are permuted
+//    (both sides of each dot product identically) so every smem read is one conflict-free
+//    LDS.128 under the 128B swizzle and P feeds the PV MMA straight from the S accumulator.
+//  * Online softmax in base 2 (exp2 of log2e-prescaled logits), row max over 4 lanes by
+//    xor-shuffles, rescale skipped warp-uniformly when no row max grew.
+//  * Each warp writes an fp32 partial (m, l, o) per (CTA, request); attn_combine_kernel
+//    merges the partials of a request with the log-sum-exp rule.
+#include <cuda_bf16.h>
+
+#include "internal.h"
+
+namespace ellm {
+namespace {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
+
+__host__ __device__ constexpr int stages_for(int D) { return D == 128 ? 3 : 6; }
+__host__ __device__ constexpr int stage_bytes_for(int D) { return 2 * 128 * D * 2; }  // HB*TT = 128
+__host__ __device__ constexpr int smem_bytes_for(int D) {
+  return stages_for(D) * stage_bytes_for(D) + 1024 /*align*/ + 2 * 8 * stages_for(D);
+}
+
+// token permutation inside a 16-token subtile: column c of the S tile holds
+// token perm16(c). perm8 = 0,5,1,4,2,7,3,6 makes the K and V smem reads bank-conflict free.
+__device__ __forceinline__ int perm8(int c) { return (c & 1) ? (4 + ((c >> 1) ^ 1)) : (c >> 1); }
+__device__ __forceinline__ int perm16(int c) { return (c & 8) | perm8(c & 7); }
+
+// 16-byte block (of a d-row) that lane-quad q reads at K instruction i.
+template <int D>
+__device__ __forceinline__ int kblock(int q, int i) {
+  if constexpr (D == 128) {
+    return ((i >> 1) << 3) | (((q >> 1) << 2) | (q & 1) | ((i & 1) << 1));
+  } else {
+    return q + 4 * i;
+  }
+}
+// 16-byte block of V that lane-group g reads for PV block k.
+template <int D>
+__device__ __forceinline__ int vblock(int g, int k) {
+  if constexpr (D == 128) return g + 8 * k;
+  else return 4 * (g & 1) + (g >> 1);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            int c3, int c4, uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar),
+      "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void mma_bf16(float* d, uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+  // rows 8..15 of A (q-heads 8..15 of a group) are unused: group <= 8 (pool_create)
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+      "{%8, %9}, {%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+struct Params {
+  const int32_t* table;
+  const int32_t* req;
+  const int32_t* len;
+  const int32_t* cum;
+  const __nv_bfloat16* q;
+  float* part;
+  float* part_ml;
+  int64_t W;
+  int32_t table_stride, n_vr, HG, G, T, L, layer, group, Hq;
+  float scale_log2;
+};
+
+// largest vr with cum[vr] <= t
+__device__ __forceinline__ int find_vr(const int32_t* cum, int n_vr, int64_t t) {
+  int lo = 0, hi = n_vr - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (__ldg(cum + mid) <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <int D, int HB>
+__global__ void __launch_bounds__(kThreads, 1)
+    paged_attn_kernel(const __grid_constant__ CUtensorMap tmap, const Params p) {
+  constexpr int TT = 128 / HB;          // stage tokens
+  constexpr int NSUB = TT / 16;         // subtiles per stage per head
+  constexpr int NST = stages_for(D);
+  constexpr int SB = stage_bytes_for(D);
+  constexpr int HALVES = D / 64;
+  constexpr int KI = D / 32;            // K blocks (16 B) per lane per token row
+  constexpr int NB = D / 64;            // V blocks per lane
+  constexpr int NT = D / 8;             // PV n-tiles
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * SB);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + NST);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int b = blockIdx.x;
+  const int64_t w0 = int64_t(b) * p.W / p.G, w1 = int64_t(b + 1) * p.W / p.G;
+  if (w0 >= w1) return;
+  const int tok_box = p.T < TT ? p.T : TT;
+  const int npieces = TT / tok_box;
+  const int piece_bytes = 2 * HB * tok_box * D * 2;
+
+  if (warp == kConsumerWarps) {
+    // ===================== producer: table walk + TMA issue =====================
+    if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    uint64_t policy;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    int stage = 0;
+    uint32_t phase = 0;
+    int vr = find_vr(p.cum, p.n_vr, w0);
+    for (int64_t tile = w0; tile < w1; ++vr) {
+      const int64_t seg_end = min(w1, int64_t(__ldg(p.cum + vr + 1)));
+      const int ireq = vr / p.HG, hg = vr % p.HG;
+      const int32_t len = __ldg(p.len + ireq);
+      const int32_t* trow = p.table + int64_t(__ldg(p.req + ireq)) * p.table_stride;
+      const int64_t tile0 = __ldg(p.cum + vr);
+      for (int64_t t = tile; t < seg_end; t += 32) {
+        const int cnt = int(min(int64_t(32), seg_end - t));
+        int32_t ent[8];
+        {
+          const int64_t tokb = (t + lane - tile0) * TT;  // first position of this lane's tile
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            ent[k] = -1;
+            if (k < npieces && lane < cnt && tokb + int64_t(k) * tok_box < len)
+              ent[k] = __ldg(trow + (tokb + int64_t(k) * tok_box) / p.T);
+          }
+        }
+        for (int u = 0; u < cnt; ++u) {
+          int32_t e[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) e[k] = __shfl_sync(0xffffffffu, ent[k], u);
+          if (lane == 0) {
+            mbar_wait(empty0 + 8 * stage, phase ^ 1);
+            int npc = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) npc += (k < npieces && e[k] >= 0);
+            mbar_expect_tx(full0 + 8 * stage, uint32_t(npc * piece_bytes));
+            const int tokoff = int(((t + u - tile0) * TT) % p.T);
+            const int tok_in_chunk = p.T >= TT ? tokoff : 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (k < npieces && e[k] >= 0)
+                tma_load_5d(sbase + stage * SB + k * piece_bytes, &tmap, 0, 0, tok_in_chunk, hg * HB,
+                            (e[k] * p.L + p.layer) * 2, full0 + 8 * stage, policy);
+          }
+          __syncwarp();
+          if (++stage == NST) { stage = 0; phase ^= 1; }
+        }
+      }
+      tile = seg_end;
+    }
+    return;
+  }
+
+  // ========================= consumers =========================
+  const int hh = warp % HB, j = warp / HB;
+  const int g = lane >> 2, q = lane & 3;
+  // smem byte offsets (within a stage) of this lane's K and V reads; fixed for the kernel
+  auto soff = [&](int kv, int tau, int blk) -> uint32_t {
+    const int piece = tau / tok_box, t = tau % tok_box;
+    const int line = ((kv * HB + hh) * tok_box + t) * HALVES + (blk >> 3);
+    return uint32_t(piece * piece_bytes + line * 128 + (((blk & 7) ^ (line & 7)) << 4));
+  };
+  uint32_t koff[2][KI], voff[4][NB];
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int i = 0; i < KI; ++i) koff[nt][i] = soff(0, 16 * j + perm16(nt * 8 + g), kblock<D>(q, i));
+  int vcol[4] = {2 * q, 2 * q + 1, 2 * q + 8, 2 * q + 9};
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int k = 0; k < NB; ++k) voff[r][k] = soff(1, 16 * j + perm16(vcol[r]), vblock<D>(g, k));
+
+  const int rows = HB * p.group;
+  int stage = 0;
+  uint32_t phase = 0;
+  int vr = find_vr(p.cum, p.n_vr, w0);
+  for (int64_t tile = w0; tile < w1; ++vr) {
+    const int64_t seg_end = min(w1, int64_t(__ldg(p.cum + vr + 1)));
+    const int ireq = vr / p.HG, hg = vr % p.HG;
+    const int32_t len = __ldg(p.len + ireq);
+    const int64_t tile0 = __ldg(p.cum + vr);
+    const int row = hh * p.group + g;  // q-head row within this head group
+    uint4 qb[KI];
+    if (g < p.group) {
+      const uint4* qrow = reinterpret_cast<const uint4*>(
+          p.q + (int64_t(ireq) * p.Hq + hg * HB * p.group + row) * D);
+#pragma unroll
+      for (int i = 0; i < KI; ++i) qb[i] = __ldg(qrow + kblock<D>(q, i));
+    } else {
+#pragma unroll
+      for (int i = 0; i < KI; ++i) qb[i] = make_uint4(0, 0, 0, 0);
+    }
+    float o[NT][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float m_run = -INFINITY, l_run = 0.f;
+
+    for (; tile < seg_end; ++tile) {
+      mbar_wait(full0 + 8 * stage, phase);
+      const uint32_t st = sbase + stage * SB;
+      const int valid = int(min(int64_t(16), int64_t(len) - ((tile - tile0) * TT + 16 * j)));
+      if (valid > 0) {
+        // ---- S = Q K^T : rows = q-heads, cols = 16 tokens (two n-tiles) ----
+        float s[2][4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+#pragma unroll
+          for (int i = 0; i < KI; ++i) {
+            const uint4 kk = lds128(st + koff[nt][i]);
+            mma_bf16(s[nt], qb[i].x, qb[i].y, kk.x, kk.y);
+            mma_bf16(s[nt], qb[i].z, qb[i].w, kk.z, kk.w);
+          }
+        }
+        // ---- online softmax (base 2) on row g ----
+        float x[2][2];
+        float mx = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            float v = s[nt][c] * p.scale_log2;
+            if (perm16(nt * 8 + 2 * q + c) >= valid) v = -INFINITY;
+            x[nt][c] = v;
+            mx = fmaxf(mx, v);
+          }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float m_new = fmaxf(m_run, mx);
+        if (__any_sync(0xffffffffu, m_new > m_run)) {
+          const float alpha = ex2(m_run - m_new);
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            o[n][0] *= alpha;
+            o[n][1] *= alpha;
+          }
+          l_run *= alpha;
+          m_run = m_new;
+        }
+        float pr[2][2];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            pr[nt][c] = ex2(x[nt][c] - m_run);
+            l_run += pr[nt][c];
+          }
+        const uint32_t pa0 = pack_bf16(pr[0][0], pr[0][1]);
+        const uint32_t pa2 = pack_bf16(pr[1][0], pr[1][1]);
+        // ---- O += P V : V rows regrouped token-pairwise with byte permutes ----
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+          uint4 v[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) v[r] = lds128(st + voff[r][k]);
+          if (valid < 16) {  // tail: never multiply garbage rows (could be Inf/NaN) by P = 0
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+              if (perm16(vcol[r]) >= valid) v[r] = make_uint4(0, 0, 0, 0);
+          }
+          const uint32_t* v0 = &v[0].x;
+          const uint32_t* v1 = &v[1].x;
+          const uint32_t* v2 = &v[2].x;
+          const uint32_t* v3 = &v[3].x;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            mma_bf16(o[8 * k + 2 * u], pa0, pa2, __byte_perm(v0[u], v1[u], 0x5410),
+                     __byte_perm(v2[u], v3[u], 0x5410));
+            mma_bf16(o[8 * k + 2 * u + 1], pa0, pa2, __byte_perm(v0[u], v1[u], 0x7632),
+                     __byte_perm(v2[u], v3[u], 0x7632));
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * stage);
+      if (++stage == NST) { stage = 0; phase ^= 1; }
+    }
+
+    // ---- partial record of (CTA b, virtual request vr, subtile slot j) ----
+    float l_tot = l_run + __shfl_xor_sync(0xffffffffu, l_run, 1);
+    l_tot += __shfl_xor_sync(0xffffffffu, l_tot, 2);
+    if (g < p.group) {
+      const int64_t rec = (int64_t(b + vr) * NSUB + j) * rows + row;
+      float* dst = p.part + rec * D;
+      if constexpr (D == 128) {
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          float4* d4 = reinterpret_cast<float4*>(dst + 64 * h2 + 16 * q);
+          d4[0] = make_float4(o[8 * h2 + 0][0], o[8 * h2 + 1][0], o[8 * h2 + 2][0], o[8 * h2 + 3][0]);
+          d4[1] = make_float4(o[8 * h2 + 4][0], o[8 * h2 + 5][0], o[8 * h2 + 6][0], o[8 * h2 + 7][0]);
+          d4[2] = make_float4(o[8 * h2 + 0][1], o[8 * h2 + 1][1], o[8 * h2 + 2][1], o[8 * h2 + 3][1]);
+          d4[3] = make_float4(o[8 * h2 + 4][1], o[8 * h2 + 5][1], o[8 * h2 + 6][1], o[8 * h2 + 7][1]);
+        }
+      } else {
+        float4* a = reinterpret_cast<float4*>(dst + 8 * q);
+        a[0] = make_float4(o[0][0], o[1][0], o[2][0], o[3][0]);
+        a[1] = make_float4(o[4][0], o[5][0], o[6][0], o[7][0]);
+        float4* c = reinterpret_cast<float4*>(dst + 32 + 8 * q);
+        c[0] = make_float4(o[0][1], o[1][1], o[2][1], o[3][1]);
+        c[1] = make_float4(o[4][1], o[5][1], o[6][1], o[7][1]);
+      }
+      if (q == 0) *reinterpret_cast<float2*>(p.part_ml + rec * 2) = make_float2(m_run, l_tot);
+    }
+  }
+}
+
+// LSE merge of the partial records of each (virtual request, q-head row) (a5).
+template <int D>
+__global__ void __launch_bounds__(D) attn_combine_kernel(
+    const float* __restrict__ part, const float* __restrict__ part_ml, const int32_t* __restrict__ b_first,
+    const int32_t* __restrict__ b_last, int32_t nsub, int32_t rows, int32_t HG, int32_t HB, int32_t group,
+    int32_t Hq, __nv_bfloat16* __restrict__ out) {
+  const int vr = blockIdx.x, row = blockIdx.y, e = threadIdx.x;
+  const int64_t p0 = int64_t(__ldg(b_first + vr) + vr) * nsub;
+  const int64_t p1 = int64_t(__ldg(b_last + vr) + vr + 1) * nsub;
+  float M = -INFINITY;
+  for (int64_t pp = p0; pp < p1; ++pp) M = fmaxf(M, __ldg(part_ml + (pp * rows + row) * 2));
+  float L = 0.f, acc = 0.f;
+  for (int64_t pp = p0; pp < p1; ++pp) {
+    const float2 ml = __ldg(reinterpret_cast<const float2*>(part_ml + (pp * rows + row) * 2));
+    const float w = ex2(ml.x - M);  // -inf partial (no valid token) -> 0
+    L += w * ml.y;
+    acc += w * __ldg(part + (pp * rows + row) * D + e);
+  }
+  const int ireq = vr / HG, hg = vr % HG;
+  out[(int64_t(ireq) * Hq + hg * HB * group + row) * D + e] = __float2bfloat16_rn(acc / L);
+}
+
+template <int D, int HB>
+cudaError_t launch_t(const CUtensorMap& tmap, const Params& prm, int G, cudaStream_t s) {
+  paged_attn_kernel<D, HB><<<G, kThreads, smem_bytes_for(D), s>>>(tmap, prm);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int attn_heads_per_block(int32_t Hkv) { return Hkv >= 8 ? 8 : Hkv; }
+int attn_stage_tokens(int32_t HB) { return 128 / HB; }
+
+template <int D>
+static cudaError_t configure_d(int32_t HB) {
+  const void* f = nullptr;
+  switch (HB) {
+    case 1: f = reinterpret_cast<const void*>(paged_attn_kernel<D, 1>); break;
+    case 2: f = reinterpret_cast<const void*>(paged_attn_kernel<D, 2>); break;
+    case 4: f = reinterpret_cast<const void*>(paged_attn_kernel<D, 4>); break;
+    case 8: f = reinterpret_cast<const void*>(paged_attn_kernel<D, 8>); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes_for(D));
+}
+
+cudaError_t attn_configure(int32_t D, int32_t HB) {
+  return D == 128 ? configure_d<128>(HB) : D == 64 ? configure_d<64>(HB) : cudaErrorInvalidValue;
+}
+
+// 5-D view of the pool: (64 elems, d/64 halves, T tokens, Hkv heads, chunk*L*2 + layer*2 + kv)
+// with the box (64, d/64, min(T,TT), HB, 2): one TMA = K and V of HB heads for up to TT tokens.
+cudaError_t encode_kv_tensor_map(CUtensorMap* map, void* pool_base, int64_t max_chunks,
+                                 const AttnShape& sh) {
+  const Driver& d = driver();
+  if (!d.ok) return cudaErrorNotSupported;
+  cuuint64_t dims[5] = {64, cuuint64_t(sh.D / 64), cuuint64_t(sh.T), cuuint64_t(sh.Hkv),
+                        cuuint64_t(max_chunks) * sh.L * 2};
+  cuuint64_t strides[4] = {128, cuuint64_t(sh.D) * 2, cuuint64_t(sh.T) * sh.D * 2,
+                           cuuint64_t(sh.Hkv) * sh.T * sh.D * 2};
+  cuuint32_t box[5] = {64, cuuint32_t(sh.D / 64), cuuint32_t(sh.T < sh.TT ? sh.T : sh.TT),
+                       cuuint32_t(sh.HB), 2};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = d.tensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, pool_base, dims, strides,
+                                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh, const AttnDesc& d,
+                                   int32_t n, int32_t n_vr, int64_t W, int32_t G,
+                                   const int32_t* table, int32_t table_stride, int32_t layer,
+                                   const void* q, void* out, float* part, float* part_ml,
+                                   float scale, cudaStream_t s, int* launches) {
+  (void)n;
+  Params prm;
+  prm.table = table;
+  prm.req = d.req;
+  prm.len = d.len;
+  prm.cum = d.cum;
+  prm.q = static_cast<const __nv_bfloat16*>(q);
+  prm.part = part;
+  prm.part_ml = part_ml;
+  prm.W = W;
+  prm.table_stride = table_stride;
+  prm.n_vr = n_vr;
+  prm.HG = sh.HG;
+  prm.G = G;
+  prm.T = sh.T;
+  prm.L = sh.L;
+  prm.layer = layer;
+  prm.group = sh.group;
+  prm.Hq = sh.Hq;
+  prm.scale_log2 = scale * 1.4426950408889634f;
+  cudaError_t e;
+  if (sh.D == 128) {
+    switch (sh.HB) {
+      case 1: e = launch_t<128, 1>(tmap, prm, G, s); break;
+      case 2: e = launch_t<128, 2>(tmap, prm, G, s); break;
+      case 4: e = launch_t<128, 4>(tmap, prm, G, s); break;
+      default: e = launch_t<128, 8>(tmap, prm, G, s); break;
+    }
+  } else {
+    switch (sh.HB) {
+      case 1: e = launch_t<64, 1>(tmap, prm, G, s); break;
+      case 2: e = launch_t<64, 2>(tmap, prm, G, s); break;
+      case 4: e = launch_t<64, 4>(tmap, prm, G, s); break;
+      default: e = launch_t<64, 8>(tmap, prm, G, s); break;
+    }
+  }
+  if (e != cudaSuccess) return e;
+  *launches = 1;
+  const int rows = sh.HB * sh.group;
+  const dim3 grid = dim3(unsigned(n_vr), unsigned(rows), 1u);
+  if (sh.D == 128)
+    attn_combine_kernel<128><<<grid, 128, 0, s>>>(part, part_ml, d.b_first, d.b_last, sh.nsub, rows, sh.HG,
+                                                 sh.HB, sh.group, sh.Hq, static_cast<__nv_bfloat16*>(out));
+  else
+    attn_combine_kernel<64><<<grid, 64, 0, s>>>(part, part_ml, d.b_first, d.b_last, sh.nsub, rows, sh.HG,
+                                               sh.HB, sh.group, sh.Hq, static_cast<__nv_bfloat16*>(out));
+  e = cudaGetLastError();
+  if (e == cudaSuccess) *launches = 2;
+  return e;
+}
+
+}  // namespace ellm

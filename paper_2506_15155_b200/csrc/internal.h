@@ -1,0 +1,179 @@
+// internal.h — private declarations of libellm.so (not part of the ABI; see include/ellm.h).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <map>
+#include <vector>
+
+#include "../../include/ellm.h"
+
+namespace ellm {
+
+// ---- driver API through the runtime's entry-point table (no -lcuda link dependency) ----
+struct Driver {
+  bool ok = false;
+  CUresult (*memAddressReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+  CUresult (*memAddressFree)(CUdeviceptr, size_t);
+  CUresult (*memCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*,
+                        unsigned long long);
+  CUresult (*memRelease)(CUmemGenericAllocationHandle);
+  CUresult (*memMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+  CUresult (*memUnmap)(CUdeviceptr, size_t);
+  CUresult (*memSetAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+  CUresult (*memGetAllocationGranularity)(size_t*, const CUmemAllocationProp*,
+                                          CUmemAllocationGranularity_flags);
+  CUresult (*tensorMapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+};
+const Driver& driver();  // loads once; .ok false if unavailable
+
+int64_t now_ns();
+
+// ---- staging ring: host-snapshot -> device small-array uploads, stream-ordered ----------
+// Pinned host + device buffers split into segments; a segment is reused only after the
+// events recorded for work that consumed it have completed.
+class StagingRing {
+ public:
+  int init(size_t seg_bytes, int n_segs);
+  void destroy();
+  // Reserve `bytes` (<= seg_bytes) and return host / device views of it.
+  int alloc(size_t bytes, void** host, void** dev, uint64_t* generation);
+  // Copy the host view of [dev, dev+bytes) to the device on `stream` (async).
+  int upload(void* dev, size_t bytes, cudaStream_t stream);
+  // Mark the segment holding `dev` as used by the work about to be enqueued.
+  void touch(const void* dev);
+  // Record that work enqueued on `stream` so far consumes every touched segment.
+  int commit(cudaStream_t stream);
+  bool still_valid(const void* dev, uint64_t generation) const;
+  size_t seg_bytes() const { return seg_bytes_; }
+
+ private:
+  struct Seg {
+    uint64_t generation = 0;
+    std::vector<cudaEvent_t> events;
+    std::vector<cudaStream_t> streams;
+  };
+  int retire_and_advance();
+  int commit_seg(int seg, cudaStream_t stream);
+  std::vector<int> touched_;
+  uint8_t* h_ = nullptr;
+  uint8_t* d_ = nullptr;
+  size_t seg_bytes_ = 0;
+  int n_segs_ = 0;
+  int cur_ = 0;
+  size_t off_ = 0;
+  std::vector<Seg> segs_;
+  std::vector<cudaEvent_t> free_events_;
+};
+
+// ---- kernel launchers (kernels.cu / attention.cu) ---------------------------------------
+struct TableUpdate {
+  int32_t index;
+  int32_t value;
+};
+cudaError_t launch_table_scatter(int32_t* d_table, const TableUpdate* d_updates, int32_t n,
+                                 cudaStream_t s);
+
+struct AppendDesc {  // device-resident arrays, n entries (+1 for cum)
+  const int32_t* req;
+  const int32_t* pos0;
+  const int32_t* cum_rows;
+};
+cudaError_t launch_kv_append(const AppendDesc& d, int32_t n, int64_t total_rows, const int32_t* table,
+                             int32_t table_stride, uint8_t* pool, int64_t chunk_bytes, int32_t T,
+                             int32_t layer, int32_t Hkv, int32_t D, const void* k_new,
+                             const void* v_new, int num_sms, cudaStream_t s);
+
+// Chunk copy: dst_base + dst_idx[i]*bytes <- src_base + src_idx[i]*bytes, i < n.
+cudaError_t launch_chunk_copy(uint8_t* dst_base, const int32_t* dst_idx, const uint8_t* src_base,
+                              const int32_t* src_idx, int32_t n, int64_t chunk_bytes, int grid,
+                              cudaStream_t s);
+
+struct AttnDesc {  // device-resident
+  const int32_t* req;      // [n]
+  const int32_t* len;      // [n]
+  const int32_t* cum;      // [n_vr + 1] tiles
+  const int32_t* b_first;  // [n_vr]
+  const int32_t* b_last;   // [n_vr]
+};
+struct AttnShape {
+  int32_t D, HB, HG, Hkv, Hq, group, T, L, TT, nsub;
+};
+int attn_heads_per_block(int32_t Hkv);  // HB
+int attn_stage_tokens(int32_t HB);      // TT
+cudaError_t attn_configure(int32_t D, int32_t HB);   // smem attributes, once
+cudaError_t encode_kv_tensor_map(CUtensorMap* map, void* pool_base, int64_t max_chunks,
+                                 const AttnShape& sh);
+cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh, const AttnDesc& d,
+                                   int32_t n, int32_t n_vr, int64_t W, int32_t G,
+                                   const int32_t* table, int32_t table_stride, int32_t layer,
+                                   const void* q, void* out, float* part, float* part_ml,
+                                   float scale, cudaStream_t s, int* launches);
+
+}  // namespace ellm
+
+// ---- the pool ---------------------------------------------------------------------------
+struct ellm_vtensor {
+  int32_t device = -1;
+  size_t slot_bytes = 0;
+  int64_t n_slots = 0;
+  CUdeviceptr base = 0;
+  std::vector<CUmemGenericAllocationHandle> handles;
+  std::vector<uint8_t> mapped;
+  int64_t n_map = 0, n_unmap = 0, map_ns = 0, unmap_ns = 0;
+};
+
+struct ellm_pool {
+  ellm_pool_config cfg{};
+  bool has_dev = false;
+  int64_t chunk_bytes = 0;
+  int32_t T = 0, group = 0;
+
+  // ownership / state: owner 0 = KV, 1 = ACT
+  std::vector<uint8_t> owner, used;
+  int64_t n_free_kv = 0, n_used_kv = 0, n_act = 0;
+  int64_t free_hint = 0;  // no FREE KV chunk below this id
+  std::vector<int32_t> chunk_req, chunk_idx;  // back-pointers of USED chunks
+  std::vector<uint8_t> hused;
+  int64_t n_host_used = 0, host_hint = 0;
+  std::vector<int32_t> slot_req, slot_idx;
+
+  // per request
+  std::vector<int32_t> table;  // [max_requests][max_chunks_per_request] host authoritative
+  std::vector<int64_t> len;
+  std::vector<int32_t> pending, nonres;
+
+  // device side
+  ellm_vtensor* vt = nullptr;        // one slot per map unit
+  int64_t unit_bytes = 0;            // bytes per physical map unit
+  int64_t chunks_per_unit = 1;       // >1 when chunk_bytes < granularity
+  std::vector<int32_t> unit_kv;      // KV-owned chunks in each unit
+  int32_t* d_table = nullptr;
+  uint8_t* host_slots = nullptr;     // pinned, mapped
+  float* d_part = nullptr;
+  float* d_part_ml = nullptr;
+  int64_t part_records = 0;
+  CUtensorMap tmap{};
+  ellm::AttnShape ash{};
+  int num_sms = 0;
+  ellm::StagingRing ring;
+  int swap_mode = 0;
+  std::vector<ellm::TableUpdate> pending_updates;
+
+  // attention descriptor cache
+  std::vector<int32_t> cache_key;     // req ids then lens
+  const int32_t* cache_dev = nullptr;
+  uint64_t cache_gen = 0;
+  int32_t cache_n_vr = 0;
+  int64_t cache_W = 0;
+  int32_t cache_G = 0;
+
+  std::map<int32_t, std::pair<CUdeviceptr, size_t>> alias;
+  int last_cuda_error = 0;
+  int64_t launches = 0;
+};

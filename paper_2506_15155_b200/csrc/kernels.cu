@@ -1,0 +1,114 @@
+// kernels.cu — sm_100a kernels for the byte-moving rows of the hot path:
+//   table_scatter   device mirror of the chunk tables (a2)
+//   kv_append       scatter new K/V rows into chunk slabs through the table (a3)
+//   chunk_copy      whole-chunk copies for deflate / inflate / migrate (a6-a8)
+// All three are HBM- (or host-link-) bound byte copies: 16-byte vector accesses, several
+// independent loads in flight per thread before the stores, grids sized to the SM count.
+#include "internal.h"
+
+namespace ellm {
+namespace {
+
+__global__ void table_scatter_kernel(int32_t* __restrict__ table, const TableUpdate* __restrict__ up,
+                                     int32_t n) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    TableUpdate u = up[i];
+    table[u.index] = u.value;
+  }
+}
+
+// One 16-byte unit per thread iteration. Unit u covers K (u < half) or V; within a half the
+// order is (row, head, part) so reads of k_new / v_new are fully coalesced, and the 16 B
+// parts of one (row, head) land contiguously in its slab row (layout [L][2][Hkv][T][d]).
+__global__ void __launch_bounds__(256) kv_append_kernel(
+    const int32_t* __restrict__ req, const int32_t* __restrict__ pos0,
+    const int32_t* __restrict__ cum_rows, int32_t n, int64_t half_units, const int32_t* __restrict__ table,
+    int32_t table_stride, uint8_t* __restrict__ pool, int64_t chunk_bytes, int32_t T, int32_t layer,
+    int32_t Hkv, int32_t parts, const uint4* __restrict__ k_new, const uint4* __restrict__ v_new) {
+  const int64_t total = 2 * half_units;
+  for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < total;
+       u += int64_t(gridDim.x) * blockDim.x) {
+    const int kv = u >= half_units;
+    const int64_t w = kv ? u - half_units : u;
+    const uint4 val = kv ? __ldg(v_new + w) : __ldg(k_new + w);
+    const int32_t part = int32_t(w % parts);
+    const int64_t rh = w / parts;
+    const int32_t h = int32_t(rh % Hkv);
+    const int32_t row = int32_t(rh / Hkv);
+    // request of this row: largest i with cum_rows[i] <= row
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (__ldg(cum_rows + mid) <= row) lo = mid; else hi = mid - 1;
+    }
+    const int32_t p = __ldg(pos0 + lo) + (row - __ldg(cum_rows + lo));
+    const int32_t c = __ldg(table + int64_t(__ldg(req + lo)) * table_stride + p / T);
+    const int64_t off = int64_t(c) * chunk_bytes +
+                        ((int64_t(layer * 2 + kv) * Hkv + h) * T + (p % T)) * int64_t(parts) * 16 +
+                        int64_t(part) * 16;
+    *reinterpret_cast<uint4*>(pool + off) = val;
+  }
+}
+
+// Whole-chunk copy. A warp moves one 4 KiB unit per iteration with 8 x 16 B loads in flight
+// per lane before its stores (latency hiding for HBM and for host memory over PCIe).
+constexpr int kCopyUnit = 4096;
+__global__ void __launch_bounds__(256) chunk_copy_kernel(uint8_t* __restrict__ dst_base,
+                                                         const int32_t* __restrict__ dst_idx,
+                                                         const uint8_t* __restrict__ src_base,
+                                                         const int32_t* __restrict__ src_idx,
+                                                         int32_t n, int64_t chunk_bytes) {
+  const int lane = threadIdx.x & 31;
+  const int64_t units_per_chunk = chunk_bytes / kCopyUnit;
+  const int64_t total = int64_t(n) * units_per_chunk;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t w = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total; w += warps) {
+    const int64_t i = w / units_per_chunk;
+    const int64_t off = (w % units_per_chunk) * kCopyUnit;
+    const uint4* s = reinterpret_cast<const uint4*>(src_base + int64_t(__ldg(src_idx + i)) * chunk_bytes + off);
+    uint4* d = reinterpret_cast<uint4*>(dst_base + int64_t(__ldg(dst_idx + i)) * chunk_bytes + off);
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldcs(s + k * 32 + lane);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) __stcs(d + k * 32 + lane, v[k]);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_table_scatter(int32_t* d_table, const TableUpdate* d_updates, int32_t n,
+                                 cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int grid = std::min<int>((n + 255) / 256, 1024);
+  table_scatter_kernel<<<grid, 256, 0, s>>>(d_table, d_updates, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kv_append(const AppendDesc& d, int32_t n, int64_t total_rows, const int32_t* table,
+                             int32_t table_stride, uint8_t* pool, int64_t chunk_bytes, int32_t T,
+                             int32_t layer, int32_t Hkv, int32_t D, const void* k_new,
+                             const void* v_new, int num_sms, cudaStream_t s) {
+  const int32_t parts = D / 8;
+  const int64_t half_units = total_rows * Hkv * parts;
+  int64_t blocks = (2 * half_units + 255) / 256;
+  int grid = int(std::min<int64_t>(blocks, int64_t(num_sms) * 8));
+  kv_append_kernel<<<grid, 256, 0, s>>>(d.req, d.pos0, d.cum_rows, n, half_units, table, table_stride,
+                                        pool, chunk_bytes, T, layer, Hkv, parts,
+                                        static_cast<const uint4*>(k_new), static_cast<const uint4*>(v_new));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chunk_copy(uint8_t* dst_base, const int32_t* dst_idx, const uint8_t* src_base,
+                              const int32_t* src_idx, int32_t n, int64_t chunk_bytes, int grid,
+                              cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  if (chunk_bytes % kCopyUnit != 0) return cudaErrorInvalidValue;
+  int64_t units = int64_t(n) * (chunk_bytes / kCopyUnit);
+  int64_t need = (units + 7) / 8;
+  grid = int(std::max<int64_t>(1, std::min<int64_t>(grid, need)));
+  chunk_copy_kernel<<<grid, 256, 0, s>>>(dst_base, dst_idx, src_base, src_idx, n, chunk_bytes);
+  return cudaGetLastError();
+}
+
+}  // namespace ellm

@@ -1,0 +1,756 @@
+// pool.cpp — host side of libellm.so: chunk pool with KV/ACT ownership, per-request
+// chunk tables (the KV eTensor's logical->physical map), pinned host slots (the CPU
+// elastic buffer), and the C-ABI entry points of include/ellm.h that drive the
+// kernels in kernels.cu / attention.cu.
+//
+// Every entry point validates all preconditions before mutating (include/ellm.h
+// "Conventions"); allocation is lowest-id-first (R7).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <set>
+
+#include "internal.h"
+
+using namespace ellm;
+
+namespace {
+
+constexpr int32_t UNMAPPED = -1;
+inline bool is_dev(int32_t e) { return e >= 0; }
+inline bool is_host(int32_t e) { return e <= -2; }
+inline int32_t host_of(int32_t e) { return -e - 2; }
+inline int32_t enc_host(int64_t h) { return int32_t(-(h + 2)); }
+constexpr uint8_t KV = 0, ACT = 1;
+
+int cuda_fail(ellm_pool* p, cudaError_t e) {
+  if (p) p->last_cuda_error = int(e);
+  return ELLM_ERR_CUDA;
+}
+
+bool has_dup(int32_t n, const int32_t* a) {
+  if (n <= 1) return false;
+  std::vector<int32_t> v(a, a + n);
+  std::sort(v.begin(), v.end());
+  return std::adjacent_find(v.begin(), v.end()) != v.end();
+}
+
+int64_t nchunks_of(const ellm_pool* p, int64_t len) { return (len + p->T - 1) / p->T; }
+int32_t& entry(ellm_pool* p, int32_t r, int64_t i) {
+  return p->table[size_t(int64_t(r) * p->cfg.max_chunks_per_request + i)];
+}
+int32_t entry_c(const ellm_pool* p, int32_t r, int64_t i) {
+  return p->table[size_t(int64_t(r) * p->cfg.max_chunks_per_request + i)];
+}
+void set_entry(ellm_pool* p, int32_t r, int64_t i, int32_t v) {
+  entry(p, r, i) = v;
+  p->pending_updates.push_back(
+      {int32_t(int64_t(r) * p->cfg.max_chunks_per_request + i), v});
+}
+
+int64_t take_lowest_free_kv(ellm_pool* p) {
+  for (int64_t c = p->free_hint; c < p->cfg.max_chunks; ++c)
+    if (p->owner[size_t(c)] == KV && !p->used[size_t(c)]) {
+      p->used[size_t(c)] = 1;
+      p->free_hint = c + 1;
+      --p->n_free_kv;
+      ++p->n_used_kv;
+      return c;
+    }
+  return -1;
+}
+void free_chunk(ellm_pool* p, int64_t c) {
+  p->used[size_t(c)] = 0;
+  p->chunk_req[size_t(c)] = -1;
+  ++p->n_free_kv;
+  --p->n_used_kv;
+  p->free_hint = std::min(p->free_hint, c);
+}
+int64_t take_lowest_free_host(ellm_pool* p) {
+  for (int64_t h = p->host_hint; h < p->cfg.host_slots; ++h)
+    if (!p->hused[size_t(h)]) {
+      p->hused[size_t(h)] = 1;
+      p->host_hint = h + 1;
+      ++p->n_host_used;
+      return h;
+    }
+  return -1;
+}
+void free_host(ellm_pool* p, int64_t h) {
+  p->hused[size_t(h)] = 0;
+  p->slot_req[size_t(h)] = -1;
+  --p->n_host_used;
+  p->host_hint = std::min(p->host_hint, h);
+}
+
+cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Upload pending table updates (snapshots of host entries) and scatter them on `stream`.
+int flush_table(ellm_pool* p, cudaStream_t stream) {
+  if (!p->has_dev) {
+    p->pending_updates.clear();
+    return ELLM_OK;
+  }
+  const size_t per = p->ring.seg_bytes() / sizeof(TableUpdate);
+  size_t done = 0;
+  while (done < p->pending_updates.size()) {
+    size_t n = std::min(per, p->pending_updates.size() - done);
+    void *h, *d;
+    int rc = p->ring.alloc(n * sizeof(TableUpdate), &h, &d, nullptr);
+    if (rc) return rc;
+    std::memcpy(h, p->pending_updates.data() + done, n * sizeof(TableUpdate));
+    if ((rc = p->ring.upload(d, n * sizeof(TableUpdate), stream))) return rc;
+    cudaError_t e = launch_table_scatter(p->d_table, static_cast<TableUpdate*>(d), int32_t(n), stream);
+    if (e != cudaSuccess) return cuda_fail(p, e);
+    ++p->launches;
+    if ((rc = p->ring.commit(stream))) return rc;
+    done += n;
+  }
+  p->pending_updates.clear();
+  return ELLM_OK;
+}
+
+// Upload an int32 array through the staging ring; returns the device pointer.
+int upload_ints(ellm_pool* p, const std::vector<int32_t>& v, cudaStream_t stream,
+                const int32_t** dev, uint64_t* gen) {
+  void *h, *d;
+  int rc = p->ring.alloc(std::max<size_t>(v.size(), 1) * 4, &h, &d, gen);
+  if (rc) return rc;
+  if (!v.empty()) std::memcpy(h, v.data(), v.size() * 4);
+  if ((rc = p->ring.upload(d, std::max<size_t>(v.size(), 1) * 4, stream))) return rc;
+  *dev = static_cast<const int32_t*>(d);
+  return ELLM_OK;
+}
+
+int map_unit_if_needed(ellm_pool* p, int64_t unit) {
+  if (!p->has_dev || p->vt->mapped[size_t(unit)]) return ELLM_OK;
+  return ellm_vtensor_map(p->vt, unit, 1);
+}
+
+bool check_reqs_range(const ellm_pool* p, int32_t n, const int32_t* r) {
+  for (int32_t i = 0; i < n; ++i)
+    if (r[i] < 0 || r[i] >= p->cfg.max_requests) return false;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ellm_status_string(int s) {
+  switch (s) {
+    case ELLM_OK: return "ok";
+    case ELLM_ERR_INVALID_ARG: return "invalid argument";
+    case ELLM_ERR_OUT_OF_RANGE: return "out of range";
+    case ELLM_ERR_NO_CHUNKS: return "not enough free KV chunks";
+    case ELLM_ERR_HOST_FULL: return "not enough free host slots";
+    case ELLM_ERR_NOT_RESIDENT: return "chunk not resident on the device";
+    case ELLM_ERR_NOT_MAPPED: return "chunk or slot not in use / not mapped";
+    case ELLM_ERR_ALREADY_MAPPED: return "destination already in use";
+    case ELLM_ERR_IN_USE: return "chunks in use";
+    case ELLM_ERR_CUDA: return "CUDA error";
+    case ELLM_ERR_NCCL: return "NCCL error";
+    case ELLM_ERR_NO_DEVICE: return "pool has no device";
+    case ELLM_ERR_UNSUPPORTED: return "unsupported shape";
+    default: return "unknown status";
+  }
+}
+
+int ellm_last_cuda_error(const ellm_pool* p) { return p ? p->last_cuda_error : 0; }
+int64_t ellm_kernel_launches(const ellm_pool* p) { return p ? p->launches : 0; }
+
+int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out) {
+  if (!cfg || !out) return ELLM_ERR_INVALID_ARG;
+  *out = nullptr;
+  const ellm_pool_config& c = *cfg;
+  if (c.n_layers <= 0 || c.n_heads_q <= 0 || c.n_heads_kv <= 0 || c.head_dim <= 0 ||
+      c.tokens_per_chunk <= 0 || c.max_chunks <= 0 || c.initial_chunks < 0 ||
+      c.initial_chunks > c.max_chunks || c.max_requests <= 0 || c.max_chunks_per_request <= 0 ||
+      c.host_slots < 0 || c.n_heads_q % c.n_heads_kv != 0 || c.max_chunks > INT32_MAX ||
+      c.host_slots > INT32_MAX - 2 ||
+      int64_t(c.max_requests) * c.max_chunks_per_request > INT32_MAX)
+    return ELLM_ERR_INVALID_ARG;
+  const int32_t T = c.tokens_per_chunk, group = c.n_heads_q / c.n_heads_kv;
+  if ((c.head_dim != 64 && c.head_dim != 128) || T < 16 || (T & (T - 1)) != 0 || group > 8 ||
+      (c.n_heads_kv & (c.n_heads_kv - 1)) != 0)
+    return ELLM_ERR_UNSUPPORTED;
+
+  ellm_pool* p = new ellm_pool();
+  p->cfg = c;
+  p->T = T;
+  p->group = group;
+  p->chunk_bytes = int64_t(4) * T * c.n_layers * c.n_heads_kv * c.head_dim;
+  p->has_dev = c.device != ELLM_DEVICE_NONE;
+  p->owner.assign(size_t(c.max_chunks), ACT);
+  p->used.assign(size_t(c.max_chunks), 0);
+  for (int64_t i = 0; i < c.initial_chunks; ++i) p->owner[size_t(i)] = KV;
+  p->n_free_kv = c.initial_chunks;
+  p->n_act = c.max_chunks - c.initial_chunks;
+  p->chunk_req.assign(size_t(c.max_chunks), -1);
+  p->chunk_idx.assign(size_t(c.max_chunks), -1);
+  p->hused.assign(size_t(c.host_slots), 0);
+  p->slot_req.assign(size_t(c.host_slots), -1);
+  p->slot_idx.assign(size_t(c.host_slots), -1);
+  p->table.assign(size_t(int64_t(c.max_requests) * c.max_chunks_per_request), UNMAPPED);
+  p->len.assign(size_t(c.max_requests), 0);
+  p->pending.assign(size_t(c.max_requests), 0);
+  p->nonres.assign(size_t(c.max_requests), 0);
+  if (!p->has_dev) {
+    *out = p;
+    return ELLM_OK;
+  }
+
+  auto fail = [&](int rc) {
+    ellm_pool_destroy(p);
+    return rc;
+  };
+  cudaError_t e;
+  if (c.device < 0 || (e = cudaSetDevice(c.device)) != cudaSuccess) return fail(ELLM_ERR_CUDA);
+  if (!driver().ok) return fail(ELLM_ERR_CUDA);
+  size_t gran = 0;
+  int rc = ellm_vmm_granularity(c.device, &gran);
+  if (rc) return fail(rc);
+  if (p->chunk_bytes % int64_t(gran) == 0) {
+    p->unit_bytes = p->chunk_bytes;
+    p->chunks_per_unit = 1;
+  } else if (int64_t(gran) % p->chunk_bytes == 0) {
+    p->unit_bytes = int64_t(gran);
+    p->chunks_per_unit = int64_t(gran) / p->chunk_bytes;
+  } else {
+    return fail(ELLM_ERR_UNSUPPORTED);
+  }
+  int64_t n_units = (c.max_chunks + p->chunks_per_unit - 1) / p->chunks_per_unit;
+  if ((rc = ellm_vtensor_create(c.device, size_t(p->unit_bytes), n_units, &p->vt))) return fail(rc);
+  p->unit_kv.assign(size_t(n_units), 0);
+  for (int64_t i = 0; i < c.initial_chunks; ++i) ++p->unit_kv[size_t(i / p->chunks_per_unit)];
+  for (int64_t u = 0; u < n_units; ++u)
+    if (p->unit_kv[size_t(u)] > 0 && (rc = ellm_vtensor_map(p->vt, u, 1))) return fail(rc);
+  if (c.host_slots > 0) {
+    if ((e = cudaHostAlloc(reinterpret_cast<void**>(&p->host_slots),
+                           size_t(c.host_slots) * size_t(p->chunk_bytes),
+                           cudaHostAllocMapped | cudaHostAllocPortable)) != cudaSuccess)
+      return fail(cuda_fail(p, e));
+  }
+  size_t tbytes = p->table.size() * 4;
+  if ((e = cudaMalloc(reinterpret_cast<void**>(&p->d_table), tbytes)) != cudaSuccess ||
+      (e = cudaMemset(p->d_table, 0xFF, tbytes)) != cudaSuccess)
+    return fail(cuda_fail(p, e));
+  cudaDeviceProp prop;
+  if ((e = cudaGetDeviceProperties(&prop, c.device)) != cudaSuccess) return fail(cuda_fail(p, e));
+  p->num_sms = prop.multiProcessorCount;
+
+  AttnShape& a = p->ash;
+  a.D = c.head_dim;
+  a.Hkv = c.n_heads_kv;
+  a.Hq = c.n_heads_q;
+  a.group = group;
+  a.HB = attn_heads_per_block(c.n_heads_kv);
+  a.HG = c.n_heads_kv / a.HB;
+  a.TT = attn_stage_tokens(a.HB);
+  a.nsub = a.TT / 16;
+  a.T = T;
+  a.L = c.n_layers;
+  // split-K partial records: pid < (G + n_vr) * nsub, each [HB*group][D] fp32 + (m, l)
+  p->part_records = (int64_t(p->num_sms) + int64_t(c.max_requests) * a.HG) * a.nsub;
+  if ((e = cudaMalloc(reinterpret_cast<void**>(&p->d_part),
+                      size_t(p->part_records) * a.HB * group * a.D * 4)) != cudaSuccess ||
+      (e = cudaMalloc(reinterpret_cast<void**>(&p->d_part_ml),
+                      size_t(p->part_records) * a.HB * group * 2 * 4)) != cudaSuccess)
+    return fail(cuda_fail(p, e));
+  if ((rc = p->ring.init(size_t(1) << 20, 16))) return fail(rc);
+  if ((e = encode_kv_tensor_map(&p->tmap, ellm_vtensor_base(p->vt), c.max_chunks, a)) != cudaSuccess)
+    return fail(cuda_fail(p, e));
+  if ((e = attn_configure(a.D, a.HB)) != cudaSuccess) return fail(cuda_fail(p, e));
+  *out = p;
+  return ELLM_OK;
+}
+
+int ellm_pool_destroy(ellm_pool* p) {
+  if (!p) return ELLM_ERR_INVALID_ARG;
+  if (p->has_dev) {
+    cudaSetDevice(p->cfg.device);
+    cudaDeviceSynchronize();
+    for (auto it = p->alias.begin(); it != p->alias.end();) {
+      int32_t r = it->first;
+      ++it;
+      ellm_unalias_request(p, r);
+    }
+    p->ring.destroy();
+    if (p->d_table) cudaFree(p->d_table);
+    if (p->d_part) cudaFree(p->d_part);
+    if (p->d_part_ml) cudaFree(p->d_part_ml);
+    if (p->host_slots) cudaFreeHost(p->host_slots);
+    if (p->vt) ellm_vtensor_destroy(p->vt);
+  }
+  delete p;
+  return ELLM_OK;
+}
+
+int ellm_pool_stats(const ellm_pool* p, ellm_stats* o) {
+  if (!p || !o) return ELLM_ERR_INVALID_ARG;
+  o->kv_free = p->n_free_kv;
+  o->kv_used = p->n_used_kv;
+  o->act = p->n_act;
+  o->host_used = p->n_host_used;
+  o->host_free = p->cfg.host_slots - p->n_host_used;
+  o->n_map = p->vt ? p->vt->n_map : 0;
+  o->n_unmap = p->vt ? p->vt->n_unmap : 0;
+  o->map_ns = p->vt ? p->vt->map_ns : 0;
+  o->unmap_ns = p->vt ? p->vt->unmap_ns : 0;
+  o->chunk_bytes = p->chunk_bytes;
+  int64_t mapped = 0;
+  if (p->vt)
+    for (uint8_t m : p->vt->mapped) mapped += m;
+  o->mapped_bytes = mapped * p->unit_bytes;
+  return ELLM_OK;
+}
+
+void* ellm_pool_base(const ellm_pool* p) { return p && p->vt ? ellm_vtensor_base(p->vt) : nullptr; }
+void* ellm_pool_host_base(const ellm_pool* p) { return p ? p->host_slots : nullptr; }
+
+int ellm_set_swap_mode(ellm_pool* p, int32_t mode) {
+  if (!p || (mode != 0 && mode != 1)) return ELLM_ERR_INVALID_ARG;
+  p->swap_mode = mode;
+  return ELLM_OK;
+}
+
+// a2 — O2 in SURVEY §8(c): on-demand chunk mapping at write, all-or-nothing.
+int ellm_kv_reserve(ellm_pool* p, int32_t n, const int32_t* reqs, const int32_t* n_new,
+                    void* stream) {
+  if (!p || n < 0 || (n > 0 && (!reqs || !n_new))) return ELLM_ERR_INVALID_ARG;
+  if (!check_reqs_range(p, n, reqs)) return ELLM_ERR_OUT_OF_RANGE;
+  if (has_dup(n, reqs)) return ELLM_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (n_new[i] < 0) return ELLM_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (nchunks_of(p, p->len[size_t(reqs[i])] + n_new[i]) > p->cfg.max_chunks_per_request)
+      return ELLM_ERR_OUT_OF_RANGE;
+  for (int32_t i = 0; i < n; ++i) {
+    int64_t L = p->len[size_t(reqs[i])];
+    if (n_new[i] > 0 && L % p->T != 0 && is_host(entry_c(p, reqs[i], L / p->T)))
+      return ELLM_ERR_NOT_RESIDENT;
+  }
+  int64_t need = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    int64_t L = p->len[size_t(reqs[i])];
+    need += nchunks_of(p, L + n_new[i]) - nchunks_of(p, L);
+  }
+  if (need > p->n_free_kv) return ELLM_ERR_NO_CHUNKS;
+  for (int32_t i = 0; i < n; ++i) {
+    int32_t r = reqs[i];
+    int64_t L = p->len[size_t(r)];
+    for (int64_t ci = nchunks_of(p, L); ci < nchunks_of(p, L + n_new[i]); ++ci) {
+      int64_t c = take_lowest_free_kv(p);
+      p->chunk_req[size_t(c)] = r;
+      p->chunk_idx[size_t(c)] = int32_t(ci);
+      set_entry(p, r, ci, int32_t(c));
+    }
+    p->len[size_t(r)] = L + n_new[i];
+    p->pending[size_t(r)] = n_new[i];
+  }
+  return flush_table(p, S(stream));
+}
+
+// a3 — O3: the KV cache grows by the generated K/V.
+int ellm_kv_append(ellm_pool* p, int32_t layer, int32_t n, const int32_t* reqs,
+                   const int32_t* n_new, const void* k_new, const void* v_new, void* stream) {
+  if (!p || n < 0 || (n > 0 && (!reqs || !n_new))) return ELLM_ERR_INVALID_ARG;
+  if (layer < 0 || layer >= p->cfg.n_layers) return ELLM_ERR_OUT_OF_RANGE;
+  if (!check_reqs_range(p, n, reqs)) return ELLM_ERR_OUT_OF_RANGE;
+  if (has_dup(n, reqs)) return ELLM_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (n_new[i] != p->pending[size_t(reqs[i])]) return ELLM_ERR_INVALID_ARG;
+  int64_t rows = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    int32_t r = reqs[i];
+    int64_t L = p->len[size_t(r)];
+    if (n_new[i] > 0)
+      for (int64_t ci = (L - n_new[i]) / p->T; ci <= (L - 1) / p->T; ++ci)
+        if (!is_dev(entry_c(p, r, ci))) return ELLM_ERR_NOT_RESIDENT;
+    rows += n_new[i];
+  }
+  if (!p->has_dev) return ELLM_ERR_NO_DEVICE;
+  if (rows == 0) return ELLM_OK;
+  if (!k_new || !v_new) return ELLM_ERR_INVALID_ARG;
+  std::vector<int32_t> d(size_t(3 * n + 1));
+  int32_t cum = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    d[size_t(i)] = reqs[i];
+    d[size_t(n + i)] = int32_t(p->len[size_t(reqs[i])] - n_new[i]);
+    d[size_t(2 * n + i)] = cum;
+    cum += n_new[i];
+  }
+  d[size_t(3 * n)] = cum;
+  const int32_t* dd;
+  int rc = upload_ints(p, d, S(stream), &dd, nullptr);
+  if (rc) return rc;
+  AppendDesc ad{dd, dd + n, dd + 2 * n};
+  cudaError_t e = launch_kv_append(ad, n, rows, p->d_table, p->cfg.max_chunks_per_request,
+                                   static_cast<uint8_t*>(ellm_vtensor_base(p->vt)), p->chunk_bytes,
+                                   p->T, layer, p->cfg.n_heads_kv, p->cfg.head_dim, k_new, v_new,
+                                   p->num_sms, S(stream));
+  if (e != cudaSuccess) return cuda_fail(p, e);
+  ++p->launches;
+  return p->ring.commit(S(stream));
+}
+
+// a4 + a5 — O4: exact softmax attention over the accumulated KV.
+int ellm_paged_decode_attention(ellm_pool* p, int32_t layer, int32_t n, const int32_t* reqs,
+                                const void* q, void* out, float scale, void* stream) {
+  if (!p || n < 0 || (n > 0 && !reqs)) return ELLM_ERR_INVALID_ARG;
+  if (layer < 0 || layer >= p->cfg.n_layers) return ELLM_ERR_OUT_OF_RANGE;
+  if (!check_reqs_range(p, n, reqs)) return ELLM_ERR_OUT_OF_RANGE;
+  for (int32_t i = 0; i < n; ++i)
+    if (p->len[size_t(reqs[i])] == 0) return ELLM_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (p->nonres[size_t(reqs[i])] > 0) return ELLM_ERR_NOT_RESIDENT;
+  if (!p->has_dev) return ELLM_ERR_NO_DEVICE;
+  if (n == 0) return ELLM_OK;
+  if (!q || !out || !std::isfinite(scale)) return ELLM_ERR_INVALID_ARG;
+  const AttnShape& a = p->ash;
+  const int32_t n_vr = n * a.HG;
+  // descriptor cache: the same batch is attended at every layer of a decode step
+  std::vector<int32_t> key(size_t(2 * n));
+  for (int32_t i = 0; i < n; ++i) {
+    key[size_t(i)] = reqs[i];
+    key[size_t(n + i)] = int32_t(p->len[size_t(reqs[i])]);
+  }
+  if (key != p->cache_key || !p->ring.still_valid(p->cache_dev, p->cache_gen)) {
+    // layout: req[n] len[n] cum[n_vr+1] b_first[n_vr] b_last[n_vr]
+    std::vector<int32_t> d(size_t(2 * n + 3 * n_vr + 1));
+    int64_t W = 0;
+    for (int32_t i = 0; i < n; ++i) {
+      d[size_t(i)] = reqs[i];
+      d[size_t(n + i)] = key[size_t(n + i)];
+    }
+    int32_t* cum = d.data() + 2 * n;
+    for (int32_t vr = 0; vr < n_vr; ++vr) {
+      cum[vr] = int32_t(W);
+      W += (p->len[size_t(reqs[vr / a.HG])] + a.TT - 1) / a.TT;
+    }
+    cum[n_vr] = int32_t(W);
+    if (W > INT32_MAX / 2) return ELLM_ERR_UNSUPPORTED;
+    // G = min(#SMs, W) persistent CTAs: every CTA then owns >= 1 tile, so every CTA in
+    // [b_first(vr), b_last(vr)] writes a partial record for vr (the combine reads exactly those).
+    const int32_t G = int32_t(std::min<int64_t>(p->num_sms, W));
+    // CTA b owns tiles [floor(b W / G), floor((b+1) W / G)); the CTA holding tile t is
+    // floor(((t+1) G - 1) / W).
+    auto cta_of = [&](int64_t t) { return int32_t(((t + 1) * G - 1) / W); };
+    for (int32_t vr = 0; vr < n_vr; ++vr) {
+      d[size_t(2 * n + n_vr + 1 + vr)] = cta_of(cum[vr]);
+      d[size_t(2 * n + 2 * n_vr + 1 + vr)] = cta_of(int64_t(cum[vr + 1]) - 1);
+    }
+    const int32_t* dd;
+    uint64_t gen;
+    int rc = upload_ints(p, d, S(stream), &dd, &gen);
+    if (rc) return rc;
+    p->cache_key = key;
+    p->cache_dev = dd;
+    p->cache_gen = gen;
+    p->cache_n_vr = n_vr;
+    p->cache_W = W;
+    p->cache_G = G;
+  } else {
+    p->ring.touch(p->cache_dev);
+  }
+  const int32_t* dd = p->cache_dev;
+  AttnDesc ad{dd, dd + n, dd + 2 * n, dd + 2 * n + n_vr + 1, dd + 2 * n + 2 * n_vr + 1};
+  int launches = 0;
+  cudaError_t e = launch_paged_attention(p->tmap, a, ad, n, n_vr, p->cache_W, p->cache_G, p->d_table,
+                                         p->cfg.max_chunks_per_request, layer, q, out, p->d_part,
+                                         p->d_part_ml, scale, S(stream), &launches);
+  p->launches += launches;
+  if (e != cudaSuccess) return cuda_fail(p, e);
+  return p->ring.commit(S(stream));
+}
+
+// O8 — released slots return to the pool.
+int ellm_release(ellm_pool* p, int32_t r, void* stream) {
+  (void)stream;
+  if (!p) return ELLM_ERR_INVALID_ARG;
+  if (r < 0 || r >= p->cfg.max_requests) return ELLM_ERR_OUT_OF_RANGE;
+  int64_t nc = nchunks_of(p, p->len[size_t(r)]);
+  for (int64_t i = 0; i < nc; ++i) {
+    int32_t e = entry_c(p, r, i);
+    if (is_dev(e)) free_chunk(p, e);
+    if (is_host(e)) free_host(p, host_of(e));
+    entry(p, r, i) = UNMAPPED;  // device mirror rows beyond len are never read
+  }
+  p->len[size_t(r)] = 0;
+  p->pending[size_t(r)] = 0;
+  p->nonres[size_t(r)] = 0;
+  if (p->alias.count(r)) ellm_unalias_request(p, r);
+  return ELLM_OK;
+}
+
+// a6 — O5: offload to CPU DRAM; deflation is the reverse of inflation.
+int ellm_deflate(ellm_pool* p, int32_t n, const int32_t* ids, int32_t* slots_out, void* stream) {
+  if (!p || n < 0 || (n > 0 && (!ids || !slots_out))) return ELLM_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (ids[i] < 0 || ids[i] >= p->cfg.max_chunks) return ELLM_ERR_OUT_OF_RANGE;
+  if (has_dup(n, ids)) return ELLM_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (p->owner[size_t(ids[i])] != KV || !p->used[size_t(ids[i])]) return ELLM_ERR_NOT_MAPPED;
+  if (n > p->cfg.host_slots - p->n_host_used) return ELLM_ERR_HOST_FULL;
+  std::vector<int32_t> src(static_cast<size_t>(n)), dst(static_cast<size_t>(n));
+  for (int32_t i = 0; i < n; ++i) {
+    int64_t c = ids[i];
+    int64_t h = take_lowest_free_host(p);
+    int32_t r = p->chunk_req[size_t(c)], ci = p->chunk_idx[size_t(c)];
+    p->slot_req[size_t(h)] = r;
+    p->slot_idx[size_t(h)] = ci;
+    set_entry(p, r, ci, enc_host(h));
+    ++p->nonres[size_t(r)];
+    free_chunk(p, c);
+    slots_out[i] = int32_t(h);
+    src[size_t(i)] = int32_t(c);
+    dst[size_t(i)] = int32_t(h);
+  }
+  if (!p->has_dev || n == 0) return flush_table(p, S(stream));
+  cudaError_t e;
+  uint8_t* pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
+  if (p->swap_mode == 1) {
+    for (int32_t i = 0; i < n; ++i)
+      if ((e = cudaMemcpyAsync(p->host_slots + int64_t(dst[size_t(i)]) * p->chunk_bytes,
+                               pool + int64_t(src[size_t(i)]) * p->chunk_bytes,
+                               size_t(p->chunk_bytes), cudaMemcpyDeviceToHost, S(stream))) !=
+          cudaSuccess)
+        return cuda_fail(p, e);
+  } else {
+    std::vector<int32_t> both(src);
+    both.insert(both.end(), dst.begin(), dst.end());
+    const int32_t* dd;
+    int rc = upload_ints(p, both, S(stream), &dd, nullptr);
+    if (rc) return rc;
+    uint8_t* hdev = nullptr;
+    if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&hdev), p->host_slots, 0)) != cudaSuccess)
+      return cuda_fail(p, e);
+    if ((e = launch_chunk_copy(hdev, dd + n, pool, dd, n, p->chunk_bytes, 2 * p->num_sms, S(stream))) !=
+        cudaSuccess)
+      return cuda_fail(p, e);
+    ++p->launches;
+  }
+  return flush_table(p, S(stream));
+}
+
+// a7 — O6: fetch when decoding is scheduled, remap onto chunks.
+int ellm_inflate(ellm_pool* p, int32_t n, const int32_t* slots, int32_t* ids_out, void* stream) {
+  if (!p || n < 0 || (n > 0 && (!slots || !ids_out))) return ELLM_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (slots[i] < 0 || slots[i] >= p->cfg.host_slots) return ELLM_ERR_OUT_OF_RANGE;
+  if (has_dup(n, slots)) return ELLM_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (!p->hused[size_t(slots[i])]) return ELLM_ERR_NOT_MAPPED;
+  if (n > p->n_free_kv) return ELLM_ERR_NO_CHUNKS;
+  std::vector<int32_t> src(static_cast<size_t>(n)), dst(static_cast<size_t>(n));
+  for (int32_t i = 0; i < n; ++i) {
+    int64_t h = slots[i];
+    int64_t c = take_lowest_free_kv(p);
+    int32_t r = p->slot_req[size_t(h)], ci = p->slot_idx[size_t(h)];
+    p->chunk_req[size_t(c)] = r;
+    p->chunk_idx[size_t(c)] = ci;
+    set_entry(p, r, ci, int32_t(c));
+    --p->nonres[size_t(r)];
+    free_host(p, h);
+    ids_out[i] = int32_t(c);
+    src[size_t(i)] = int32_t(h);
+    dst[size_t(i)] = int32_t(c);
+  }
+  if (!p->has_dev || n == 0) return flush_table(p, S(stream));
+  cudaError_t e;
+  uint8_t* pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
+  if (p->swap_mode == 1) {
+    for (int32_t i = 0; i < n; ++i)
+      if ((e = cudaMemcpyAsync(pool + int64_t(dst[size_t(i)]) * p->chunk_bytes,
+                               p->host_slots + int64_t(src[size_t(i)]) * p->chunk_bytes,
+                               size_t(p->chunk_bytes), cudaMemcpyHostToDevice, S(stream))) !=
+          cudaSuccess)
+        return cuda_fail(p, e);
+  } else {
+    std::vector<int32_t> both(src);
+    both.insert(both.end(), dst.begin(), dst.end());
+    const int32_t* dd;
+    int rc = upload_ints(p, both, S(stream), &dd, nullptr);
+    if (rc) return rc;
+    uint8_t* hdev = nullptr;
+    if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&hdev), p->host_slots, 0)) != cudaSuccess)
+      return cuda_fail(p, e);
+    if ((e = launch_chunk_copy(pool, dd + n, hdev, dd, n, p->chunk_bytes, 2 * p->num_sms, S(stream))) !=
+        cudaSuccess)
+      return cuda_fail(p, e);
+    ++p->launches;
+  }
+  return flush_table(p, S(stream));
+}
+
+// a8 — O7: D2D migration (BJ north_star; the paper's own migration is ownership-only).
+int ellm_migrate(ellm_pool* p, int32_t n, const int32_t* src, const int32_t* dst, void* stream) {
+  if (!p || n < 0 || (n > 0 && (!src || !dst))) return ELLM_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (src[i] < 0 || src[i] >= p->cfg.max_chunks) return ELLM_ERR_OUT_OF_RANGE;
+  for (int32_t i = 0; i < n; ++i)
+    if (dst[i] < 0 || dst[i] >= p->cfg.max_chunks) return ELLM_ERR_OUT_OF_RANGE;
+  std::vector<int32_t> all(src, src + n);
+  all.insert(all.end(), dst, dst + n);
+  if (has_dup(int32_t(all.size()), all.data())) return ELLM_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (p->owner[size_t(src[i])] != KV || !p->used[size_t(src[i])]) return ELLM_ERR_NOT_MAPPED;
+  for (int32_t i = 0; i < n; ++i) {
+    if (p->owner[size_t(dst[i])] != KV) return ELLM_ERR_NOT_MAPPED;
+    if (p->used[size_t(dst[i])]) return ELLM_ERR_ALREADY_MAPPED;
+  }
+  for (int32_t i = 0; i < n; ++i) {
+    int64_t s = src[i], d = dst[i];
+    int32_t r = p->chunk_req[size_t(s)], ci = p->chunk_idx[size_t(s)];
+    p->used[size_t(d)] = 1;
+    --p->n_free_kv;
+    ++p->n_used_kv;
+    p->chunk_req[size_t(d)] = r;
+    p->chunk_idx[size_t(d)] = ci;
+    set_entry(p, r, ci, int32_t(d));
+    free_chunk(p, s);
+  }
+  if (!p->has_dev || n == 0) return flush_table(p, S(stream));
+  const int32_t* dd;
+  int rc = upload_ints(p, all, S(stream), &dd, nullptr);
+  if (rc) return rc;
+  uint8_t* pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
+  cudaError_t e = launch_chunk_copy(pool, dd + n, pool, dd, n, p->chunk_bytes, 2 * p->num_sms, S(stream));
+  if (e != cudaSuccess) return cuda_fail(p, e);
+  ++p->launches;
+  return flush_table(p, S(stream));
+}
+
+// a9 — inflation (3)-(4): ACT -> KV ownership transfer + on-demand remap.
+int ellm_pool_grow(ellm_pool* p, int64_t n) {
+  if (!p || n < 0) return ELLM_ERR_INVALID_ARG;
+  if (n > p->n_act) return ELLM_ERR_NO_CHUNKS;
+  std::vector<int64_t> ids;
+  for (int64_t c = 0; c < p->cfg.max_chunks && int64_t(ids.size()) < n; ++c)
+    if (p->owner[size_t(c)] == ACT) ids.push_back(c);
+  if (p->has_dev) {  // map first so a driver failure leaves ownership unchanged
+    std::set<int64_t> units;
+    for (int64_t c : ids) units.insert(c / p->chunks_per_unit);
+    for (int64_t u : units) {
+      int rc = map_unit_if_needed(p, u);
+      if (rc) return rc;
+    }
+  }
+  for (int64_t c : ids) {
+    p->owner[size_t(c)] = KV;
+    p->used[size_t(c)] = 0;
+    if (p->has_dev) ++p->unit_kv[size_t(c / p->chunks_per_unit)];
+    ++p->n_free_kv;
+    --p->n_act;
+    p->free_hint = std::min(p->free_hint, c);
+  }
+  return ELLM_OK;
+}
+
+// a9 — deflation, "the reverse process": highest-id FREE KV chunks -> ACT, and
+// physical memory whose chunks are all ACT is unmapped.
+int ellm_pool_shrink(ellm_pool* p, int64_t n) {
+  if (!p || n < 0) return ELLM_ERR_INVALID_ARG;
+  if (n > p->n_free_kv) return ELLM_ERR_IN_USE;
+  std::vector<int64_t> units;
+  for (int64_t c = p->cfg.max_chunks - 1; c >= 0 && n > 0; --c)
+    if (p->owner[size_t(c)] == KV && !p->used[size_t(c)]) {
+      p->owner[size_t(c)] = ACT;
+      --p->n_free_kv;
+      ++p->n_act;
+      --n;
+      int64_t u = c / p->chunks_per_unit;
+      if (p->has_dev && --p->unit_kv[size_t(u)] == 0) units.push_back(u);
+    }
+  if (p->has_dev)
+    for (int64_t u : units) {
+      int rc = ellm_vtensor_unmap(p->vt, u, 1);
+      if (rc) return rc;
+    }
+  return ELLM_OK;
+}
+
+int ellm_get_table(const ellm_pool* p, int32_t r, int32_t* entries, int32_t cap, int32_t* n_out,
+                   int32_t* len_out) {
+  if (!p) return ELLM_ERR_INVALID_ARG;
+  if (r < 0 || r >= p->cfg.max_requests) return ELLM_ERR_OUT_OF_RANGE;
+  int64_t nc = nchunks_of(p, p->len[size_t(r)]);
+  if (n_out) *n_out = int32_t(nc);
+  if (len_out) *len_out = int32_t(p->len[size_t(r)]);
+  for (int64_t i = 0; i < nc && i < cap; ++i) entries[i] = entry_c(p, r, i);
+  return ELLM_OK;
+}
+
+int ellm_read_chunk(ellm_pool* p, int64_t c, void* host_dst, void* stream) {
+  if (!p || !host_dst) return ELLM_ERR_INVALID_ARG;
+  if (c < 0 || c >= p->cfg.max_chunks) return ELLM_ERR_OUT_OF_RANGE;
+  if (!p->has_dev) return ELLM_ERR_NO_DEVICE;
+  if (p->owner[size_t(c)] != KV) return ELLM_ERR_NOT_MAPPED;
+  cudaError_t e;
+  const uint8_t* src = static_cast<const uint8_t*>(ellm_vtensor_base(p->vt)) + c * p->chunk_bytes;
+  if ((e = cudaMemcpyAsync(host_dst, src, size_t(p->chunk_bytes), cudaMemcpyDeviceToHost, S(stream))) !=
+          cudaSuccess ||
+      (e = cudaStreamSynchronize(S(stream))) != cudaSuccess)
+    return cuda_fail(p, e);
+  return ELLM_OK;
+}
+
+int ellm_read_host_slot(ellm_pool* p, int64_t h, void* host_dst) {
+  if (!p || !host_dst) return ELLM_ERR_INVALID_ARG;
+  if (h < 0 || h >= p->cfg.host_slots) return ELLM_ERR_OUT_OF_RANGE;
+  if (!p->has_dev) return ELLM_ERR_NO_DEVICE;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(p, e);
+  std::memcpy(host_dst, p->host_slots + h * p->chunk_bytes, size_t(p->chunk_bytes));
+  return ELLM_OK;
+}
+
+// The paper's literal KV eTensor: the request's physical chunks mapped, in logical order,
+// into one contiguous VA span, using multi-mapping of a handle.
+int ellm_alias_request(ellm_pool* p, int32_t r, void** out) {
+  if (!p || !out) return ELLM_ERR_INVALID_ARG;
+  if (r < 0 || r >= p->cfg.max_requests) return ELLM_ERR_OUT_OF_RANGE;
+  if (!p->has_dev) return ELLM_ERR_NO_DEVICE;
+  if (p->chunks_per_unit != 1) return ELLM_ERR_UNSUPPORTED;
+  if (p->alias.count(r)) return ELLM_ERR_ALREADY_MAPPED;
+  int64_t nc = nchunks_of(p, p->len[size_t(r)]);
+  if (nc == 0) return ELLM_ERR_INVALID_ARG;
+  if (p->nonres[size_t(r)] > 0) return ELLM_ERR_NOT_RESIDENT;
+  const Driver& d = driver();
+  size_t bytes = size_t(nc) * size_t(p->chunk_bytes);
+  CUdeviceptr va = 0;
+  if (d.memAddressReserve(&va, bytes, size_t(p->unit_bytes), 0, 0) != CUDA_SUCCESS) return ELLM_ERR_CUDA;
+  for (int64_t i = 0; i < nc; ++i) {
+    int32_t c = entry_c(p, r, i);
+    if (d.memMap(va + CUdeviceptr(i) * p->chunk_bytes, size_t(p->chunk_bytes), 0,
+                 p->vt->handles[size_t(c)], 0) != CUDA_SUCCESS) {
+      for (int64_t j = 0; j < i; ++j) d.memUnmap(va + CUdeviceptr(j) * p->chunk_bytes, size_t(p->chunk_bytes));
+      d.memAddressFree(va, bytes);
+      return ELLM_ERR_CUDA;
+    }
+  }
+  CUmemAccessDesc acc;
+  std::memset(&acc, 0, sizeof(acc));
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = p->cfg.device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  if (d.memSetAccess(va, bytes, &acc, 1) != CUDA_SUCCESS) return ELLM_ERR_CUDA;
+  p->alias[r] = {va, bytes};
+  *out = reinterpret_cast<void*>(va);
+  return ELLM_OK;
+}
+
+int ellm_unalias_request(ellm_pool* p, int32_t r) {
+  if (!p) return ELLM_ERR_INVALID_ARG;
+  auto it = p->alias.find(r);
+  if (it == p->alias.end()) return ELLM_ERR_NOT_MAPPED;
+  cudaDeviceSynchronize();
+  const Driver& d = driver();
+  const size_t cb = size_t(p->chunk_bytes);
+  for (size_t off = 0; off < it->second.second; off += cb) d.memUnmap(it->second.first + off, cb);
+  d.memAddressFree(it->second.first, it->second.second);
+  p->alias.erase(it);
+  return ELLM_OK;
+}
+
+}  // extern "C"
