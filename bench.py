@@ -35,13 +35,15 @@ FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback (only
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ellm", "reference"], default="ellm")
     ap.add_argument("--workload", choices=["c2", "c4"], default="c2")
     ap.add_argument("--no-swap", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="wrap the timed steps in cudaProfilerStart/Stop (ncu --profile-from-start off)")
     return ap.parse_args()
 
 
@@ -67,13 +69,19 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", self.gpu_id, "--query-gpu=" + ",".join(self.FIELDS),
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
             self.proc = None
         return self
+
+    def wait_first_sample(self, timeout=5.0):
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.02)
+        self.lines.clear()
 
     def _read(self):
         for ln in self.proc.stdout:
@@ -154,14 +162,19 @@ def run_reference(args):
     if rank != 0:
         return
     from inputs import workload as W
+    import oracle
     wl = W.c2() if args.workload == "c2" else W.c4()
-    per_rl, reps, threads = oracle_sample(wl, min_seconds=2.0)
+    k, v = W.host_kv(wl, 0, 0, wl.context)
+    q = W.host_q(wl, 0, 0)
+    scale = 1.0 / (wl.head_dim ** 0.5)
+    threads = oracle.num_threads()
     step_times = []
     for _ in range(args.warmup):
-        oracle_sample(wl, min_seconds=0.0)
-    for _ in range(args.steps):
-        t, _, _ = oracle_sample(wl, min_seconds=0.0)
-        step_times.append(t * wl.n_layers * wl.batch)
+        oracle.attention_contig(q, k, v, scale)
+    for _ in range(args.steps):  # each step: one request x one layer, scaled to the workload
+        t0 = time.perf_counter()
+        oracle.attention_contig(q, k, v, scale)
+        step_times.append((time.perf_counter() - t0) * wl.n_layers * wl.batch)
     step = statistics.mean(step_times)
     value = wl.batch / step
     cb = cpu_baseline_obj(wl, step / (wl.n_layers * wl.batch), args.steps, threads)
@@ -261,11 +274,16 @@ def main():
     launches0 = pool.kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(gpu_id_for(local)) as clk:
+        clk.wait_first_sample()
+        if args.profile:
+            torch.cuda.profiler.start()
         ev0.record(stream)
         for s in range(args.warmup, n_steps):
             step(*inputs[s], record=True)
         ev1.record(stream)
         barrier()
+        if args.profile:
+            torch.cuda.profiler.stop()
     launches = pool.kernel_launches() - launches0
     el_ms = ev0.elapsed_time(ev1)
     attn_ms = [a.elapsed_time(b) for a, b in attn_ev]

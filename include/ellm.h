@@ -183,6 +183,10 @@ int ellm_set_swap_mode(ellm_pool* pool, int32_t mode);
 /* table of req: entries[0 .. n_out) for the ceil(len/T) live logical chunks. */
 int ellm_get_table(const ellm_pool* pool, int32_t req_id, int32_t* entries, int32_t cap,
                    int32_t* n_out, int32_t* len_out);
+/* states of chunks [first, first+n): out[i] = ELLM_CHUNK_FREE (KV-owned, mapped, unused),
+ * ELLM_CHUNK_USED (referenced by a table) or ELLM_CHUNK_ACT (activation-owned / unmapped). */
+enum { ELLM_CHUNK_FREE = 0, ELLM_CHUNK_USED = 1, ELLM_CHUNK_ACT = 2 };
+int ellm_chunk_states(const ellm_pool* pool, int64_t first, int64_t n, uint8_t* out);
 /* copy chunk_bytes of device chunk `chunk_id` to host_dst (synchronises `stream`). */
 int ellm_read_chunk(ellm_pool* pool, int64_t chunk_id, void* host_dst, void* stream);
 /* copy chunk_bytes of host slot `slot` to host_dst (synchronises the device). */

@@ -167,9 +167,22 @@ def decode_inputs(wl: Workload, step: int, lens):
     return q, k, v
 
 
-def host_kv(wl: Workload, r: int, layer: int, length: int):
-    """numpy (K, V) [length, Hkv_local, d] bf16 bits of request r — the same bits the device
-    generator writes (used by the oracle side of the full-size parity checks)."""
+def host_kv(wl: Workload, r: int, layer: int, length: int, via_device: bool | None = None):
+    """numpy (K, V) [length, Hkv_local, d] bf16 bits of request r (the oracle side of the
+    full-size parity checks). Drawn by inputs/gen.py, or — for long contexts, where numpy takes
+    tens of seconds — by its bit-identical CUDA twin inputs/gen.cu (pinned against gen.py in
+    tests/test_gpu_parity.py). Either way the values come from the input generator, never from
+    the product path."""
+    if via_device is None:
+        via_device = length * wl.hkv_local * wl.head_dim > (1 << 24)
+    if via_device:
+        import torch
+        out = []
+        for kv in (0, 1):
+            t = torch.empty((length, wl.hkv_local, wl.head_dim), dtype=torch.bfloat16, device="cuda")
+            gen_kv_device(wl, r, 0, length, layer, kv, t.data_ptr(), torch.cuda.current_stream().cuda_stream)
+            out.append(np_bits(t))
+        return out[0], out[1]
     from inputs import gen
     heads = range(wl.kv_head0, wl.kv_head0 + wl.hkv_local)
     return gen.request_kv(wl.seed, r, length, layer, heads, wl.head_dim, wl.group, wl.needle_range)

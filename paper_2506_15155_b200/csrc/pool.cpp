@@ -681,6 +681,16 @@ int ellm_get_table(const ellm_pool* p, int32_t r, int32_t* entries, int32_t cap,
   return ELLM_OK;
 }
 
+int ellm_chunk_states(const ellm_pool* p, int64_t first, int64_t n, uint8_t* out) {
+  if (!p || n < 0 || (n > 0 && !out)) return ELLM_ERR_INVALID_ARG;
+  if (first < 0 || first + n > p->cfg.max_chunks) return ELLM_ERR_OUT_OF_RANGE;
+  for (int64_t i = 0; i < n; ++i) {
+    const size_t c = size_t(first + i);
+    out[i] = p->owner[c] == ACT ? ELLM_CHUNK_ACT : p->used[c] ? ELLM_CHUNK_USED : ELLM_CHUNK_FREE;
+  }
+  return ELLM_OK;
+}
+
 int ellm_read_chunk(ellm_pool* p, int64_t c, void* host_dst, void* stream) {
   if (!p || !host_dst) return ELLM_ERR_INVALID_ARG;
   if (c < 0 || c >= p->cfg.max_chunks) return ELLM_ERR_OUT_OF_RANGE;

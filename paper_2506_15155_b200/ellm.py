@@ -70,6 +70,7 @@ _SIGS = {
     "ellm_pool_shrink": (ctypes.c_int, [_P, _I64]),
     "ellm_set_swap_mode": (ctypes.c_int, [_P, _I32]),
     "ellm_get_table": (ctypes.c_int, [_P, _I32, _P, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
+    "ellm_chunk_states": (ctypes.c_int, [_P, _I64, _I64, _P]),
     "ellm_read_chunk": (ctypes.c_int, [_P, _I64, _V, _V]),
     "ellm_read_host_slot": (ctypes.c_int, [_P, _I64, _V]),
     "ellm_alias_request": (ctypes.c_int, [_P, _I32, ctypes.POINTER(_V)]),
@@ -206,6 +207,18 @@ class Pool:
         if rc != OK:
             raise EllmError(rc, "ellm_get_table")
         return ent[: n.value].copy(), ln.value
+
+    def chunk_states(self) -> np.ndarray:
+        """uint8 [max_chunks]: 0 FREE, 1 USED, 2 ACT."""
+        out = np.zeros(self.cfg.max_chunks, np.uint8)
+        rc = ellm_chunk_states(self._h, 0, self.cfg.max_chunks, _ptr(out))
+        if rc != OK:
+            raise EllmError(rc, "ellm_chunk_states")
+        return out
+
+    def free_chunks(self) -> list[int]:
+        """FREE KV chunk ids, ascending."""
+        return np.flatnonzero(self.chunk_states() == 0).tolist()
 
     def read_chunk(self, c, stream=None) -> np.ndarray:
         buf = np.zeros(self.chunk_bytes, np.uint8)
