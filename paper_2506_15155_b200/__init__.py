@@ -2,6 +2,13 @@
 
 The product is libellm.so (include/ellm.h): chunk pool + vtensor (VMM), chunk tables,
 kv_append, paged decode attention, deflate / inflate / migrate. ``ellm`` is its ctypes
-binding; ``shard`` holds the KV-head sharding helpers for N GPUs.
+binding (importing it raises if libellm.so is missing: there is no CPU fallback);
+``shard`` holds the KV-head sharding helpers for N GPUs; ``build`` compiles the library.
 """
-from . import ellm  # noqa: F401  (raises ImportError if libellm.so is missing)
+import importlib
+
+
+def __getattr__(name):
+    if name in ("ellm", "shard", "build"):
+        return importlib.import_module(f"{__name__}.{name}")
+    raise AttributeError(name)
