@@ -223,8 +223,12 @@ def main():
     wl = W.c2(world, rank) if args.workload == "c2" else W.c4(world, rank)
     B, L = wl.batch, wl.n_layers
     swap_chunks = 1024 if not args.no_swap else 0
+    t_create = time.perf_counter()
     pool = W.make_pool(wl, local, host_slots=swap_chunks)
-    W.prefill(pool, wl)
+    t_create = time.perf_counter() - t_create
+    st_create = pool.stats()
+    prefill_appends = []
+    W.prefill(pool, wl, append_times=prefill_appends)
     reqs = list(range(B))
     ones = [1] * B
     scale = 1.0 / (wl.head_dim ** 0.5)
@@ -239,19 +243,26 @@ def main():
         if world > 1 else None
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
-    attn_ev = []
+    attn_ev, app_ev, reserve_s = [], [], []
 
     def step(q, k, v, record=False):
+        t0 = time.perf_counter()
         rc = pool.reserve(reqs, ones, sp)
+        if record:
+            reserve_s.append(time.perf_counter() - t0)
         if rc:
             raise ellm.EllmError(rc, "reserve")
         for l in range(L):
+            if record:
+                a0 = torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
             rc = pool.append(l, reqs, ones, k[l], v[l], sp)
             if rc:
                 raise ellm.EllmError(rc, "append")
             if record:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
+                app_ev.append((a0, e0))
             rc = pool.attention(l, reqs, q[l], out[l], scale, sp)
             if rc:
                 raise ellm.EllmError(rc, "attention")
@@ -346,6 +357,34 @@ def main():
 
     swap = measure_swap(pool, wl, stream) if swap_chunks else None
 
+    # ---- the other §8(a) rows: reserve (a2), append (a3), VMM create / grow / shrink (a1, a9) ----
+    app_us = statistics.mean(a.elapsed_time(b) for a, b in app_ev) * 1e3
+    bulk_s = sum(t for t, _ in prefill_appends)
+    bulk_b = sum(nb for _, nb in prefill_appends)
+    peak = hbm_peak()[0]
+    st0 = pool.stats()
+    n_vmm = min(256, st0["kv_free"])
+    t0 = time.perf_counter()
+    assert pool.shrink(n_vmm) == ellm.OK
+    t_shrink = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    assert pool.grow(n_vmm) == ellm.OK
+    t_grow = time.perf_counter() - t0
+    st1 = pool.stats()
+    rows = {
+        "a1_pool_create": {"s": round(t_create, 3), "chunks_mapped": st_create["n_map"],
+                           "map_us_per_chunk": round(st_create["map_ns"] / max(1, st_create["n_map"]) / 1e3, 2),
+                           "mapped_gib": round(st_create["mapped_bytes"] / 2 ** 30, 2)},
+        "a2_kv_reserve": {"host_us_per_call": round(statistics.mean(reserve_s) * 1e6, 2), "requests": B},
+        "a3_kv_append": {"decode_us_per_call": round(app_us, 2),
+                         "decode_bytes_per_call": 2 * 2 * B * wl.hkv_local * wl.head_dim * 2,
+                         "bulk_gbs": round(bulk_b / bulk_s / 1e9, 1), "bulk_frac": round(bulk_b / bulk_s / 1e9 / peak, 3),
+                         "bulk_calls": len(prefill_appends), "bulk_bytes_per_call": int(bulk_b / len(prefill_appends))},
+        "a9_pool_shrink_grow": {"chunks": n_vmm, "shrink_ms": round(t_shrink * 1e3, 2), "grow_ms": round(t_grow * 1e3, 2),
+                                "unmap_us_per_chunk": round((st1["unmap_ns"] - st0["unmap_ns"]) / max(1, n_vmm) / 1e3, 2),
+                                "map_us_per_chunk": round((st1["map_ns"] - st0["map_ns"]) / max(1, n_vmm) / 1e3, 2)},
+    }
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         per_rl, reps, threads = oracle_sample(wl)
@@ -358,7 +397,8 @@ def main():
                 "data": "synthetic (seeded counter-based generator, 3 needles per request/layer/kv-head)",
                 "config": workload_config(wl, world), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk.summary(),
-                "attention_gbs": round(achieved, 1), "attention_frac_of_peak": roof["frac"], "swap": swap}
+                "attention_gbs": round(achieved, 1), "attention_frac_of_peak": roof["frac"], "swap": swap,
+                "rows": rows}
         print(json.dumps(line), flush=True)
     pool.close()
     if dist:

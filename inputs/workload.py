@@ -121,9 +121,10 @@ def gen_q_device(wl: Workload, r: int, layer: int, out_ptr: int, stream=0):
         raise RuntimeError("ellm_gen_q failed")
 
 
-def prefill(pool, wl: Workload, requests_per_batch: int | None = None):
+def prefill(pool, wl: Workload, requests_per_batch: int | None = None, append_times: list | None = None):
     """Reserve `context` tokens for every request and append all layers' K/V through
-    ellm_kv_append (bulk, prefill-sized appends), generated on the device."""
+    ellm_kv_append (bulk, prefill-sized appends), generated on the device. If `append_times`
+    is a list, (seconds, bytes moved) of every append call is appended to it."""
     import torch
     from paper_2506_15155_b200 import ellm
     B, n, Hkv, d = wl.batch, wl.context, wl.hkv_local, wl.head_dim
@@ -142,10 +143,18 @@ def prefill(pool, wl: Workload, requests_per_batch: int | None = None):
             for i, r in enumerate(rs):
                 gen_kv_device(wl, r, 0, n, layer, 0, kbuf.data_ptr() + i * n * row_bytes, s)
                 gen_kv_device(wl, r, 0, n, layer, 1, vbuf.data_ptr() + i * n * row_bytes, s)
+            if append_times is not None:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
             rc = pool.append(layer, rs, [n] * len(rs), kbuf, vbuf, s)
             if rc != ellm.OK:
                 raise ellm.EllmError(rc, f"prefill append layer {layer}")
+            if append_times is not None:
+                e1.record()
+                append_times.append((e0, e1, 2 * 2 * len(rs) * n * Hkv * d * 2))  # K,V x read+write
     torch.cuda.synchronize()
+    if append_times is not None:
+        append_times[:] = [(a.elapsed_time(b) / 1e3, nb) for a, b, nb in append_times]
 
 
 def decode_inputs(wl: Workload, step: int, lens):

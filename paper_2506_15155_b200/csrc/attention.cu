@@ -19,8 +19,9 @@
 //    LDS.128 under the 128B swizzle and P feeds the PV MMA straight from the S accumulator.
 //  * Online softmax in base 2 (exp2 of log2e-prescaled logits), row max over 4 lanes by
 //    xor-shuffles, rescale skipped warp-uniformly when no row max grew.
-//  * Each warp writes an fp32 partial (m, l, o) per (CTA, request); attn_combine_kernel
-//    merges the partials of a request with the log-sum-exp rule.
+//  * Each warp writes an fp32 partial (m, l, o) per (CTA, request); the last CTA to finish a
+//    request (per-request arrival counter) merges its partials with the log-sum-exp rule and
+//    writes the bf16 output, so one launch does rows a4 and a5.
 #include <cuda_bf16.h>
 
 #include "internal.h"
@@ -116,13 +117,65 @@ struct Params {
   const int32_t* req;
   const int32_t* len;
   const int32_t* cum;
+  const int32_t* b_first;  // static owners of vr: CTAs [b_first, b_last] (empty if b_last < b_first)
+  const int32_t* b_last;
+  const int32_t* u_first;  // dynamic owners of vr: units [u_first, u_last] (empty if u_last < u_first)
+  const int32_t* u_last;
+  int32_t* arrivals;       // per virtual request, zero between launches
+  unsigned long long* ticket;  // dynamic-unit ticket counter (monotone across launches)
+  unsigned long long ticket_base;
   const __nv_bfloat16* q;
+  __nv_bfloat16* out;
   float* part;
   float* part_ml;
-  int64_t W;
+  int64_t W, W_s, U, n_dyn;  // tiles; static tiles; tiles per dynamic unit; dynamic units
+  int32_t rec_dyn;           // record owner id of dynamic unit 0 (= G + n_vr)
   int32_t table_stride, n_vr, HG, G, T, L, layer, group, Hq;
   float scale_log2;
 };
+constexpr int kFirst = 1, kLast = 2, kDone = 4;  // stage metadata flags
+
+// LSE merge of the partial records of virtual request vr, run by the 256
+// consumer threads of the last CTA to finish it:
+//   M = max_p m_p,  L = sum_p 2^(m_p - M) l_p,  o = sum_p 2^(m_p - M) o_p / L   -> bf16 (RNE).
+// Records of other SMs are read through L2 (__ldcg): L1 is not coherent across SMs.
+template <int D>
+__device__ __forceinline__ void merge_request(const Params& p, int vr, int rows, int nsub, int HB) {
+  // record ranges: static owners (CTAs b) then dynamic owners (units u); record id of
+  // (owner, vr) is owner + vr, each with nsub subtile slots
+  const int64_t s0 = int64_t(__ldg(p.b_first + vr) + vr) * nsub;
+  const int64_t s1 = int64_t(__ldg(p.b_last + vr) + vr + 1) * nsub;
+  const int64_t d0 = int64_t(p.rec_dyn + __ldg(p.u_first + vr) + vr) * nsub;
+  const int64_t d1 = int64_t(p.rec_dyn + __ldg(p.u_last + vr) + vr + 1) * nsub;
+  const int ireq = vr / p.HG, hg = vr % p.HG;
+  for (int item = threadIdx.x; item < rows * (D / 4); item += kConsumerWarps * 32) {
+    const int row = item / (D / 4), e4 = item % (D / 4);
+    float M = -INFINITY;
+    for (int64_t pp = s0; pp < s1; ++pp) M = fmaxf(M, __ldcg(p.part_ml + (pp * rows + row) * 2));
+    for (int64_t pp = d0; pp < d1; ++pp) M = fmaxf(M, __ldcg(p.part_ml + (pp * rows + row) * 2));
+    float L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto add = [&](int64_t pp) {
+      const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.part_ml + (pp * rows + row) * 2));
+      const float w = ex2(ml.x - M);  // a record with no valid token has m = -inf -> weight 0
+      const float4 o = __ldcg(reinterpret_cast<const float4*>(p.part + (pp * rows + row) * D) + e4);
+      L += w * ml.y;
+      acc.x += w * o.x;
+      acc.y += w * o.y;
+      acc.z += w * o.z;
+      acc.w += w * o.w;
+    };
+    for (int64_t pp = s0; pp < s1; ++pp) add(pp);
+    for (int64_t pp = d0; pp < d1; ++pp) add(pp);
+    const float inv = 1.f / L;
+    __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+    __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+    uint2 v;
+    v.x = *reinterpret_cast<uint32_t*>(&lo);
+    v.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(p.out + (int64_t(ireq) * p.Hq + hg * HB * p.group + row) * D + 4 * e4) = v;
+  }
+}
 
 // largest vr with cum[vr] <= t
 __device__ __forceinline__ int find_vr(const int32_t* cum, int n_vr, int64_t t) {
@@ -147,6 +200,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int NT = D / 8;             // PV n-tiles
 
   extern __shared__ uint8_t smem_raw[];
+  __shared__ int s_last;
+  __shared__ int4 s_meta[NST];          // per stage: {vr, tile within vr, record owner, flags}
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * SB);
   const uint32_t sbase = smem_u32(smem);
@@ -164,61 +219,92 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
 
   const int b = blockIdx.x;
-  const int64_t w0 = int64_t(b) * p.W / p.G, w1 = int64_t(b + 1) * p.W / p.G;
-  if (w0 >= w1) return;
   const int tok_box = p.T < TT ? p.T : TT;
   const int npieces = TT / tok_box;
   const int piece_bytes = 2 * HB * tok_box * D * 2;
 
   if (warp == kConsumerWarps) {
-    // ===================== producer: table walk + TMA issue =====================
+    // ===================== producer: work claim + table walk + TMA issue =====================
     if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
     uint64_t policy;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
     int stage = 0;
     uint32_t phase = 0;
-    int vr = find_vr(p.cum, p.n_vr, w0);
-    for (int64_t tile = w0; tile < w1; ++vr) {
-      const int64_t seg_end = min(w1, int64_t(__ldg(p.cum + vr + 1)));
-      const int ireq = vr / p.HG, hg = vr % p.HG;
-      const int32_t len = __ldg(p.len + ireq);
-      const int32_t* trow = p.table + int64_t(__ldg(p.req + ireq)) * p.table_stride;
-      const int64_t tile0 = __ldg(p.cum + vr);
-      for (int64_t t = tile; t < seg_end; t += 32) {
-        const int cnt = int(min(int64_t(32), seg_end - t));
-        int32_t ent[8];
-        {
-          const int64_t tokb = (t + lane - tile0) * TT;  // first position of this lane's tile
+    // Ranges of the flat tile space this CTA streams: first its static share of the first W_s
+    // tiles, then dynamic U-tile units claimed from a ticket counter (the next ticket is
+    // requested before the current unit is streamed, hiding the atomic's latency). `owner`
+    // names the partial records a range produces: record of (owner, vr) = owner + vr, unique
+    // along the monotone staircase of (owner, request) pairs.
+    int64_t t_begin = int64_t(b) * p.W_s / p.G, t_end = int64_t(b + 1) * p.W_s / p.G;
+    int owner = b;
+    unsigned long long next_ticket = 0;
+    if (p.n_dyn > 0 && lane == 0) next_ticket = atomicAdd(p.ticket, 1ull);
+    for (;;) {
+      int vr = find_vr(p.cum, p.n_vr, t_begin);
+      for (int64_t tile = t_begin; tile < t_end; ++vr) {
+        const int64_t seg_end = min(t_end, int64_t(__ldg(p.cum + vr + 1)));
+        const int ireq = vr / p.HG, hg = vr % p.HG;
+        const int32_t len = __ldg(p.len + ireq);
+        const int32_t* trow = p.table + int64_t(__ldg(p.req + ireq)) * p.table_stride;
+        const int64_t tile0 = __ldg(p.cum + vr);
+        {  // warm L1 with this segment's Q rows for the consumers (they read them at FIRST)
+          const char* qb = reinterpret_cast<const char*>(p.q + (int64_t(ireq) * p.Hq + hg * HB * p.group) * D);
+          for (int off = lane * 128; off < HB * p.group * D * 2; off += 32 * 128)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(qb + off));
+        }
+        for (int64_t t = tile; t < seg_end; t += 32) {
+          const int cnt = int(min(int64_t(32), seg_end - t));
+          int32_t ent[8];
+          {
+            const int64_t tokb = (t + lane - tile0) * TT;  // first position of this lane's tile
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            ent[k] = -1;
-            if (k < npieces && lane < cnt && tokb + int64_t(k) * tok_box < len)
-              ent[k] = __ldg(trow + (tokb + int64_t(k) * tok_box) / p.T);
+            for (int k = 0; k < 8; ++k) {
+              ent[k] = -1;
+              if (k < npieces && lane < cnt && tokb + int64_t(k) * tok_box < len)
+                ent[k] = __ldg(trow + (tokb + int64_t(k) * tok_box) / p.T);
+            }
+          }
+          for (int u = 0; u < cnt; ++u) {
+            int32_t e[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) e[k] = __shfl_sync(0xffffffffu, ent[k], u);
+            if (lane == 0) {
+              mbar_wait(empty0 + 8 * stage, phase ^ 1);
+              const int64_t tl = t + u;
+              s_meta[stage] = make_int4(vr, int(tl - tile0), owner + vr,
+                                        (tl == tile ? kFirst : 0) | (tl == seg_end - 1 ? kLast : 0));
+              int npc = 0;
+#pragma unroll
+              for (int k = 0; k < 8; ++k) npc += (k < npieces && e[k] >= 0);
+              mbar_expect_tx(full0 + 8 * stage, uint32_t(npc * piece_bytes));
+              const int tokoff = int(((tl - tile0) * TT) % p.T);
+              const int tok_in_chunk = p.T >= TT ? tokoff : 0;
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                if (k < npieces && e[k] >= 0)
+                  tma_load_5d(sbase + stage * SB + k * piece_bytes, &tmap, 0, 0, tok_in_chunk, hg * HB,
+                              (e[k] * p.L + p.layer) * 2, full0 + 8 * stage, policy);
+            }
+            __syncwarp();
+            if (++stage == NST) { stage = 0; phase ^= 1; }
           }
         }
-        for (int u = 0; u < cnt; ++u) {
-          int32_t e[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) e[k] = __shfl_sync(0xffffffffu, ent[k], u);
-          if (lane == 0) {
-            mbar_wait(empty0 + 8 * stage, phase ^ 1);
-            int npc = 0;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) npc += (k < npieces && e[k] >= 0);
-            mbar_expect_tx(full0 + 8 * stage, uint32_t(npc * piece_bytes));
-            const int tokoff = int(((t + u - tile0) * TT) % p.T);
-            const int tok_in_chunk = p.T >= TT ? tokoff : 0;
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-              if (k < npieces && e[k] >= 0)
-                tma_load_5d(sbase + stage * SB + k * piece_bytes, &tmap, 0, 0, tok_in_chunk, hg * HB,
-                            (e[k] * p.L + p.layer) * 2, full0 + 8 * stage, policy);
-          }
-          __syncwarp();
-          if (++stage == NST) { stage = 0; phase ^= 1; }
-        }
+        tile = seg_end;
       }
-      tile = seg_end;
+      // next range: the unit of the prefetched ticket (one failing ticket per CTA ends it)
+      if (p.n_dyn == 0) break;
+      const int64_t u = int64_t(__shfl_sync(0xffffffffu, next_ticket, 0) - p.ticket_base);
+      if (u >= p.n_dyn) break;
+      if (lane == 0) next_ticket = atomicAdd(p.ticket, 1ull);
+      t_begin = p.W_s + u * p.U;
+      t_end = min(p.W, t_begin + p.U);
+      owner = p.rec_dyn + int(u);
+    }
+    // no more work: publish DONE through the next stage (plain arrive, no bytes)
+    if (lane == 0) {
+      mbar_wait(empty0 + 8 * stage, phase ^ 1);
+      s_meta[stage] = make_int4(0, 0, 0, kDone);
+      mbar_arrive(full0 + 8 * stage);
     }
     return;
   }
@@ -244,116 +330,119 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int k = 0; k < NB; ++k) voff[r][k] = soff(1, 16 * j + perm16(vcol[r]), vblock<D>(g, k));
 
   const int rows = HB * p.group;
+  const int row = hh * p.group + g;  // q-head row within a head group
   int stage = 0;
   uint32_t phase = 0;
-  int vr = find_vr(p.cum, p.n_vr, w0);
-  for (int64_t tile = w0; tile < w1; ++vr) {
-    const int64_t seg_end = min(w1, int64_t(__ldg(p.cum + vr + 1)));
-    const int ireq = vr / p.HG, hg = vr % p.HG;
-    const int32_t len = __ldg(p.len + ireq);
-    const int64_t tile0 = __ldg(p.cum + vr);
-    const int row = hh * p.group + g;  // q-head row within this head group
-    uint4 qb[KI];
-    if (g < p.group) {
-      const uint4* qrow = reinterpret_cast<const uint4*>(
-          p.q + (int64_t(ireq) * p.Hq + hg * HB * p.group + row) * D);
+  uint4 qb[KI];
+  float o[NT][4];
+  float m_run = -INFINITY, l_run = 0.f;
+  int32_t len = 0;
+  for (;;) {
+    mbar_wait(full0 + 8 * stage, phase);
+    const int4 meta = s_meta[stage];
+    if (meta.w & kDone) break;
+    const int vr = meta.x;
+    if (meta.w & kFirst) {  // a new (owner, request) segment: its Q and fresh softmax state
+      const int ireq = vr / p.HG, hg = vr % p.HG;
+      len = __ldg(p.len + ireq);
+      if (g < p.group) {
+        const uint4* qrow = reinterpret_cast<const uint4*>(
+            p.q + (int64_t(ireq) * p.Hq + hg * HB * p.group + row) * D);
 #pragma unroll
-      for (int i = 0; i < KI; ++i) qb[i] = __ldg(qrow + kblock<D>(q, i));
-    } else {
+        for (int i = 0; i < KI; ++i) qb[i] = __ldg(qrow + kblock<D>(q, i));
+      } else {
 #pragma unroll
-      for (int i = 0; i < KI; ++i) qb[i] = make_uint4(0, 0, 0, 0);
+        for (int i = 0; i < KI; ++i) qb[i] = make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+      m_run = -INFINITY;
+      l_run = 0.f;
     }
-    float o[NT][4];
+    const uint32_t st = sbase + stage * SB;
+    const int valid = int(min(int64_t(16), int64_t(len) - (int64_t(meta.y) * TT + 16 * j)));
+    if (valid > 0) {
+      // ---- S = Q K^T : rows = q-heads, cols = 16 tokens (two n-tiles) ----
+      float s[2][4];
 #pragma unroll
-    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-    float m_run = -INFINITY, l_run = 0.f;
-
-    for (; tile < seg_end; ++tile) {
-      mbar_wait(full0 + 8 * stage, phase);
-      const uint32_t st = sbase + stage * SB;
-      const int valid = int(min(int64_t(16), int64_t(len) - ((tile - tile0) * TT + 16 * j)));
-      if (valid > 0) {
-        // ---- S = Q K^T : rows = q-heads, cols = 16 tokens (two n-tiles) ----
-        float s[2][4];
+      for (int nt = 0; nt < 2; ++nt) {
+        s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
-#pragma unroll
-          for (int i = 0; i < KI; ++i) {
-            const uint4 kk = lds128(st + koff[nt][i]);
-            mma_bf16(s[nt], qb[i].x, qb[i].y, kk.x, kk.y);
-            mma_bf16(s[nt], qb[i].z, qb[i].w, kk.z, kk.w);
-          }
-        }
-        // ---- online softmax (base 2) on row g ----
-        float x[2][2];
-        float mx = -INFINITY;
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            float v = s[nt][c] * p.scale_log2;
-            if (perm16(nt * 8 + 2 * q + c) >= valid) v = -INFINITY;
-            x[nt][c] = v;
-            mx = fmaxf(mx, v);
-          }
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float m_new = fmaxf(m_run, mx);
-        if (__any_sync(0xffffffffu, m_new > m_run)) {
-          const float alpha = ex2(m_run - m_new);
-#pragma unroll
-          for (int n = 0; n < NT; ++n) {
-            o[n][0] *= alpha;
-            o[n][1] *= alpha;
-          }
-          l_run *= alpha;
-          m_run = m_new;
-        }
-        float pr[2][2];
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            pr[nt][c] = ex2(x[nt][c] - m_run);
-            l_run += pr[nt][c];
-          }
-        const uint32_t pa0 = pack_bf16(pr[0][0], pr[0][1]);
-        const uint32_t pa2 = pack_bf16(pr[1][0], pr[1][1]);
-        // ---- O += P V : V rows regrouped token-pairwise with byte permutes ----
-#pragma unroll
-        for (int k = 0; k < NB; ++k) {
-          uint4 v[4];
-#pragma unroll
-          for (int r = 0; r < 4; ++r) v[r] = lds128(st + voff[r][k]);
-          if (valid < 16) {  // tail: never multiply garbage rows (could be Inf/NaN) by P = 0
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-              if (perm16(vcol[r]) >= valid) v[r] = make_uint4(0, 0, 0, 0);
-          }
-          const uint32_t* v0 = &v[0].x;
-          const uint32_t* v1 = &v[1].x;
-          const uint32_t* v2 = &v[2].x;
-          const uint32_t* v3 = &v[3].x;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            mma_bf16(o[8 * k + 2 * u], pa0, pa2, __byte_perm(v0[u], v1[u], 0x5410),
-                     __byte_perm(v2[u], v3[u], 0x5410));
-            mma_bf16(o[8 * k + 2 * u + 1], pa0, pa2, __byte_perm(v0[u], v1[u], 0x7632),
-                     __byte_perm(v2[u], v3[u], 0x7632));
-          }
+        for (int i = 0; i < KI; ++i) {
+          const uint4 kk = lds128(st + koff[nt][i]);
+          mma_bf16(s[nt], qb[i].x, qb[i].y, kk.x, kk.y);
+          mma_bf16(s[nt], qb[i].z, qb[i].w, kk.z, kk.w);
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty0 + 8 * stage);
-      if (++stage == NST) { stage = 0; phase ^= 1; }
+      // ---- online softmax (base 2) on row g ----
+      float x[2][2];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          float v = s[nt][c] * p.scale_log2;
+          if (perm16(nt * 8 + 2 * q + c) >= valid) v = -INFINITY;
+          x[nt][c] = v;
+          mx = fmaxf(mx, v);
+        }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      const float m_new = fmaxf(m_run, mx);
+      if (__any_sync(0xffffffffu, m_new > m_run)) {
+        const float alpha = ex2(m_run - m_new);
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          o[n][0] *= alpha;
+          o[n][1] *= alpha;
+        }
+        l_run *= alpha;
+        m_run = m_new;
+      }
+      float pr[2][2];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          pr[nt][c] = ex2(x[nt][c] - m_run);
+          l_run += pr[nt][c];
+        }
+      const uint32_t pa0 = pack_bf16(pr[0][0], pr[0][1]);
+      const uint32_t pa2 = pack_bf16(pr[1][0], pr[1][1]);
+      // ---- O += P V : V rows regrouped token-pairwise with byte permutes ----
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        uint4 v[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) v[r] = lds128(st + voff[r][k]);
+        if (valid < 16) {  // tail: never multiply garbage rows (could be Inf/NaN) by P = 0
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            if (perm16(vcol[r]) >= valid) v[r] = make_uint4(0, 0, 0, 0);
+        }
+        const uint32_t* v0 = &v[0].x;
+        const uint32_t* v1 = &v[1].x;
+        const uint32_t* v2 = &v[2].x;
+        const uint32_t* v3 = &v[3].x;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          mma_bf16(o[8 * k + 2 * u], pa0, pa2, __byte_perm(v0[u], v1[u], 0x5410),
+                   __byte_perm(v2[u], v3[u], 0x5410));
+          mma_bf16(o[8 * k + 2 * u + 1], pa0, pa2, __byte_perm(v0[u], v1[u], 0x7632),
+                   __byte_perm(v2[u], v3[u], 0x7632));
+        }
+      }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * stage);
+    if (++stage == NST) { stage = 0; phase ^= 1; }
+    if (!(meta.w & kLast)) continue;
 
-    // ---- partial record of (CTA b, virtual request vr, subtile slot j) ----
+    // ---- partial record of (owner, virtual request vr, subtile slot j) ----
     float l_tot = l_run + __shfl_xor_sync(0xffffffffu, l_run, 1);
     l_tot += __shfl_xor_sync(0xffffffffu, l_tot, 2);
     if (g < p.group) {
-      const int64_t rec = (int64_t(b + vr) * NSUB + j) * rows + row;
+      const int64_t rec = (int64_t(meta.z) * NSUB + j) * rows + row;
       float* dst = p.part + rec * D;
       if constexpr (D == 128) {
 #pragma unroll
@@ -374,29 +463,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (q == 0) *reinterpret_cast<float2*>(p.part_ml + rec * 2) = make_float2(m_run, l_tot);
     }
+    // ---- arrival: the last owner to finish request vr merges its records (a5, fused) ----
+    __threadfence();  // publish this lane's records at GPU scope before the arrival
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+    if (threadIdx.x == 0) {
+      const int bf = __ldg(p.b_first + vr), bl = __ldg(p.b_last + vr);
+      const int uf = __ldg(p.u_first + vr), ul = __ldg(p.u_last + vr);
+      const int owners = (bl >= bf ? bl - bf + 1 : 0) + (ul >= uf ? ul - uf + 1 : 0);
+      const int old = atomicAdd(p.arrivals + vr, 1);
+      s_last = (old == owners - 1);
+      if (s_last) p.arrivals[vr] = 0;  // every owner of vr has arrived: re-arm for the next launch
+      __threadfence();
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+    if (s_last) merge_request<D>(p, vr, rows, NSUB, HB);
   }
-}
-
-// LSE merge of the partial records of each (virtual request, q-head row) (a5).
-template <int D>
-__global__ void __launch_bounds__(D) attn_combine_kernel(
-    const float* __restrict__ part, const float* __restrict__ part_ml, const int32_t* __restrict__ b_first,
-    const int32_t* __restrict__ b_last, int32_t nsub, int32_t rows, int32_t HG, int32_t HB, int32_t group,
-    int32_t Hq, __nv_bfloat16* __restrict__ out) {
-  const int vr = blockIdx.x, row = blockIdx.y, e = threadIdx.x;
-  const int64_t p0 = int64_t(__ldg(b_first + vr) + vr) * nsub;
-  const int64_t p1 = int64_t(__ldg(b_last + vr) + vr + 1) * nsub;
-  float M = -INFINITY;
-  for (int64_t pp = p0; pp < p1; ++pp) M = fmaxf(M, __ldg(part_ml + (pp * rows + row) * 2));
-  float L = 0.f, acc = 0.f;
-  for (int64_t pp = p0; pp < p1; ++pp) {
-    const float2 ml = __ldg(reinterpret_cast<const float2*>(part_ml + (pp * rows + row) * 2));
-    const float w = ex2(ml.x - M);  // -inf partial (no valid token) -> 0
-    L += w * ml.y;
-    acc += w * __ldg(part + (pp * rows + row) * D + e);
-  }
-  const int ireq = vr / HG, hg = vr % HG;
-  out[(int64_t(ireq) * Hq + hg * HB * group + row) * D + e] = __float2bfloat16_rn(acc / L);
 }
 
 template <int D, int HB>
@@ -447,20 +528,33 @@ cudaError_t encode_kv_tensor_map(CUtensorMap* map, void* pool_base, int64_t max_
 }
 
 cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh, const AttnDesc& d,
-                                   int32_t n, int32_t n_vr, int64_t W, int32_t G,
+                                   int32_t n, int32_t n_vr, const AttnPlan& plan,
                                    const int32_t* table, int32_t table_stride, int32_t layer,
                                    const void* q, void* out, float* part, float* part_ml,
-                                   float scale, cudaStream_t s, int* launches) {
+                                   int32_t* arrivals, float scale, cudaStream_t s, int* launches) {
   (void)n;
+  const int32_t G = plan.G;
   Params prm;
   prm.table = table;
   prm.req = d.req;
   prm.len = d.len;
   prm.cum = d.cum;
+  prm.b_first = d.b_first;
+  prm.b_last = d.b_last;
+  prm.u_first = d.u_first;
+  prm.u_last = d.u_last;
+  prm.arrivals = arrivals;
+  prm.ticket = plan.ticket;
+  prm.ticket_base = plan.ticket_base;
   prm.q = static_cast<const __nv_bfloat16*>(q);
+  prm.out = static_cast<__nv_bfloat16*>(out);
   prm.part = part;
   prm.part_ml = part_ml;
-  prm.W = W;
+  prm.W = plan.W;
+  prm.W_s = plan.W_s;
+  prm.U = plan.U;
+  prm.n_dyn = plan.n_dyn;
+  prm.rec_dyn = G + n_vr;
   prm.table_stride = table_stride;
   prm.n_vr = n_vr;
   prm.HG = sh.HG;
@@ -487,18 +581,7 @@ cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh,
       default: e = launch_t<64, 8>(tmap, prm, G, s); break;
     }
   }
-  if (e != cudaSuccess) return e;
-  *launches = 1;
-  const int rows = sh.HB * sh.group;
-  const dim3 grid = dim3(unsigned(n_vr), unsigned(rows), 1u);
-  if (sh.D == 128)
-    attn_combine_kernel<128><<<grid, 128, 0, s>>>(part, part_ml, d.b_first, d.b_last, sh.nsub, rows, sh.HG,
-                                                 sh.HB, sh.group, sh.Hq, static_cast<__nv_bfloat16*>(out));
-  else
-    attn_combine_kernel<64><<<grid, 64, 0, s>>>(part, part_ml, d.b_first, d.b_last, sh.nsub, rows, sh.HG,
-                                               sh.HB, sh.group, sh.Hq, static_cast<__nv_bfloat16*>(out));
-  e = cudaGetLastError();
-  if (e == cudaSuccess) *launches = 2;
+  *launches = e == cudaSuccess ? 1 : 0;
   return e;
 }
 

@@ -98,22 +98,33 @@ struct AttnDesc {  // device-resident
   const int32_t* req;      // [n]
   const int32_t* len;      // [n]
   const int32_t* cum;      // [n_vr + 1] tiles
-  const int32_t* b_first;  // [n_vr]
+  const int32_t* b_first;  // [n_vr] static owner CTAs of vr (empty if last < first)
   const int32_t* b_last;   // [n_vr]
+  const int32_t* u_first;  // [n_vr] dynamic owner units of vr (empty if last < first)
+  const int32_t* u_last;   // [n_vr]
+};
+// Schedule of one attention launch over W stage-tiles: the first W_s are split statically over
+// G CTAs, the rest in n_dyn units of U tiles claimed with a ticket counter.
+struct AttnPlan {
+  int64_t W = 0, W_s = 0, U = 1, n_dyn = 0;
+  int32_t G = 0;
+  unsigned long long* ticket = nullptr;
+  unsigned long long ticket_base = 0;
 };
 struct AttnShape {
   int32_t D, HB, HG, Hkv, Hq, group, T, L, TT, nsub;
 };
+constexpr int64_t kMaxDynUnits = 4096;   // cap on dynamic units per attention launch
 int attn_heads_per_block(int32_t Hkv);  // HB
 int attn_stage_tokens(int32_t HB);      // TT
 cudaError_t attn_configure(int32_t D, int32_t HB);   // smem attributes, once
 cudaError_t encode_kv_tensor_map(CUtensorMap* map, void* pool_base, int64_t max_chunks,
                                  const AttnShape& sh);
 cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh, const AttnDesc& d,
-                                   int32_t n, int32_t n_vr, int64_t W, int32_t G,
+                                   int32_t n, int32_t n_vr, const AttnPlan& plan,
                                    const int32_t* table, int32_t table_stride, int32_t layer,
                                    const void* q, void* out, float* part, float* part_ml,
-                                   float scale, cudaStream_t s, int* launches);
+                                   int32_t* arrivals, float scale, cudaStream_t s, int* launches);
 
 }  // namespace ellm
 
@@ -157,6 +168,7 @@ struct ellm_pool {
   uint8_t* host_slots = nullptr;     // pinned, mapped
   float* d_part = nullptr;
   float* d_part_ml = nullptr;
+  int32_t* d_arrivals = nullptr;     // per virtual request, for the fused split-K merge
   int64_t part_records = 0;
   CUtensorMap tmap{};
   ellm::AttnShape ash{};
@@ -170,8 +182,9 @@ struct ellm_pool {
   const int32_t* cache_dev = nullptr;
   uint64_t cache_gen = 0;
   int32_t cache_n_vr = 0;
-  int64_t cache_W = 0;
-  int32_t cache_G = 0;
+  ellm::AttnPlan cache_plan;
+  unsigned long long* d_ticket = nullptr;  // dynamic-unit ticket counter (device)
+  uint64_t ticket_base = 0;                // tickets consumed by earlier launches
 
   std::map<int32_t, std::pair<CUdeviceptr, size_t>> alias;
   int last_cuda_error = 0;

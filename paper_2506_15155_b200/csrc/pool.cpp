@@ -251,11 +251,16 @@ int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out) {
   a.T = T;
   a.L = c.n_layers;
   // split-K partial records: pid < (G + n_vr) * nsub, each [HB*group][D] fp32 + (m, l)
-  p->part_records = (int64_t(p->num_sms) + int64_t(c.max_requests) * a.HG) * a.nsub;
+  p->part_records = (int64_t(p->num_sms) + 2 * int64_t(c.max_requests) * a.HG + kMaxDynUnits) * a.nsub;
   if ((e = cudaMalloc(reinterpret_cast<void**>(&p->d_part),
                       size_t(p->part_records) * a.HB * group * a.D * 4)) != cudaSuccess ||
       (e = cudaMalloc(reinterpret_cast<void**>(&p->d_part_ml),
-                      size_t(p->part_records) * a.HB * group * 2 * 4)) != cudaSuccess)
+                      size_t(p->part_records) * a.HB * group * 2 * 4)) != cudaSuccess ||
+      (e = cudaMalloc(reinterpret_cast<void**>(&p->d_arrivals),
+                      size_t(c.max_requests) * a.HG * 4)) != cudaSuccess ||
+      (e = cudaMemset(p->d_arrivals, 0, size_t(c.max_requests) * a.HG * 4)) != cudaSuccess ||
+      (e = cudaMalloc(reinterpret_cast<void**>(&p->d_ticket), 8)) != cudaSuccess ||
+      (e = cudaMemset(p->d_ticket, 0, 8)) != cudaSuccess)
     return fail(cuda_fail(p, e));
   if ((rc = p->ring.init(size_t(1) << 20, 16))) return fail(rc);
   if ((e = encode_kv_tensor_map(&p->tmap, ellm_vtensor_base(p->vt), c.max_chunks, a)) != cudaSuccess)
@@ -279,6 +284,8 @@ int ellm_pool_destroy(ellm_pool* p) {
     if (p->d_table) cudaFree(p->d_table);
     if (p->d_part) cudaFree(p->d_part);
     if (p->d_part_ml) cudaFree(p->d_part_ml);
+    if (p->d_arrivals) cudaFree(p->d_arrivals);
+    if (p->d_ticket) cudaFree(p->d_ticket);
     if (p->host_slots) cudaFreeHost(p->host_slots);
     if (p->vt) ellm_vtensor_destroy(p->vt);
   }
@@ -416,8 +423,8 @@ int ellm_paged_decode_attention(ellm_pool* p, int32_t layer, int32_t n, const in
     key[size_t(n + i)] = int32_t(p->len[size_t(reqs[i])]);
   }
   if (key != p->cache_key || !p->ring.still_valid(p->cache_dev, p->cache_gen)) {
-    // layout: req[n] len[n] cum[n_vr+1] b_first[n_vr] b_last[n_vr]
-    std::vector<int32_t> d(size_t(2 * n + 3 * n_vr + 1));
+    // layout: req[n] len[n] cum[n_vr+1] b_first[n_vr] b_last[n_vr] u_first[n_vr] u_last[n_vr]
+    std::vector<int32_t> d(size_t(2 * n + 5 * n_vr + 1));
     int64_t W = 0;
     for (int32_t i = 0; i < n; ++i) {
       d[size_t(i)] = reqs[i];
@@ -430,15 +437,46 @@ int ellm_paged_decode_attention(ellm_pool* p, int32_t layer, int32_t n, const in
     }
     cum[n_vr] = int32_t(W);
     if (W > INT32_MAX / 2) return ELLM_ERR_UNSUPPORTED;
-    // G = min(#SMs, W) persistent CTAs: every CTA then owns >= 1 tile, so every CTA in
-    // [b_first(vr), b_last(vr)] writes a partial record for vr (the combine reads exactly those).
-    const int32_t G = int32_t(std::min<int64_t>(p->num_sms, W));
-    // CTA b owns tiles [floor(b W / G), floor((b+1) W / G)); the CTA holding tile t is
-    // floor(((t+1) G - 1) / W).
-    auto cta_of = [&](int64_t t) { return int32_t(((t + 1) * G - 1) / W); };
+    AttnPlan& pl = p->cache_plan;
+    pl.W = W;
+    if (W >= 4 * int64_t(p->num_sms)) {
+      // static share: 7/8 of the tiles, balanced over one CTA per SM; dynamic tail: the rest in
+      // units of >= 8 tiles claimed by whichever CTA is free first (absorbs the per-SM spread)
+      pl.G = p->num_sms;
+      pl.W_s = W - W / 8;
+      pl.U = std::max<int64_t>(8, (W - pl.W_s + kMaxDynUnits - 1) / kMaxDynUnits);
+      pl.n_dyn = (W - pl.W_s + pl.U - 1) / pl.U;
+    } else {
+      // small batch: G = min(#SMs, W) static CTAs, every one owning >= 1 tile
+      pl.G = int32_t(std::min<int64_t>(p->num_sms, W));
+      pl.W_s = W;
+      pl.U = 1;
+      pl.n_dyn = 0;
+    }
+    // Static CTA b owns tiles [floor(b W_s / G), floor((b+1) W_s / G)); the CTA holding tile t is
+    // floor(((t+1) G - 1) / W_s). Dynamic unit u owns [W_s + u U, W_s + (u+1) U).
+    const int64_t G = pl.G, Ws = pl.W_s;
+    auto cta_of = [&](int64_t t) { return int32_t(((t + 1) * G - 1) / Ws); };
+    int32_t* bf = d.data() + 2 * n + n_vr + 1;
+    int32_t* bl = bf + n_vr;
+    int32_t* uf = bl + n_vr;
+    int32_t* ul = uf + n_vr;
     for (int32_t vr = 0; vr < n_vr; ++vr) {
-      d[size_t(2 * n + n_vr + 1 + vr)] = cta_of(cum[vr]);
-      d[size_t(2 * n + 2 * n_vr + 1 + vr)] = cta_of(int64_t(cum[vr + 1]) - 1);
+      const int64_t t0 = cum[vr], t1 = cum[vr + 1];  // [t0, t1)
+      if (t0 < Ws) {
+        bf[vr] = cta_of(t0);
+        bl[vr] = cta_of(std::min(t1, Ws) - 1);
+      } else {
+        bf[vr] = 0;
+        bl[vr] = -1;
+      }
+      if (t1 > Ws) {
+        uf[vr] = int32_t((std::max(t0, Ws) - Ws) / pl.U);
+        ul[vr] = int32_t((t1 - 1 - Ws) / pl.U);
+      } else {
+        uf[vr] = 0;
+        ul[vr] = -1;
+      }
     }
     const int32_t* dd;
     uint64_t gen;
@@ -448,19 +486,22 @@ int ellm_paged_decode_attention(ellm_pool* p, int32_t layer, int32_t n, const in
     p->cache_dev = dd;
     p->cache_gen = gen;
     p->cache_n_vr = n_vr;
-    p->cache_W = W;
-    p->cache_G = G;
   } else {
     p->ring.touch(p->cache_dev);
   }
   const int32_t* dd = p->cache_dev;
-  AttnDesc ad{dd, dd + n, dd + 2 * n, dd + 2 * n + n_vr + 1, dd + 2 * n + 2 * n_vr + 1};
+  AttnDesc ad{dd, dd + n, dd + 2 * n, dd + 2 * n + n_vr + 1, dd + 2 * n + 2 * n_vr + 1,
+              dd + 2 * n + 3 * n_vr + 1, dd + 2 * n + 4 * n_vr + 1};
+  AttnPlan plan = p->cache_plan;
+  plan.ticket = p->d_ticket;
+  plan.ticket_base = p->ticket_base;
   int launches = 0;
-  cudaError_t e = launch_paged_attention(p->tmap, a, ad, n, n_vr, p->cache_W, p->cache_G, p->d_table,
+  cudaError_t e = launch_paged_attention(p->tmap, a, ad, n, n_vr, plan, p->d_table,
                                          p->cfg.max_chunks_per_request, layer, q, out, p->d_part,
-                                         p->d_part_ml, scale, S(stream), &launches);
+                                         p->d_part_ml, p->d_arrivals, scale, S(stream), &launches);
   p->launches += launches;
   if (e != cudaSuccess) return cuda_fail(p, e);
+  if (plan.n_dyn > 0) p->ticket_base += uint64_t(plan.n_dyn) + uint64_t(plan.G);  // tickets consumed
   return p->ring.commit(S(stream));
 }
 

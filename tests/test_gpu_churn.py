@@ -19,8 +19,8 @@ pytestmark = pytest.mark.gpu
 def test_c5_churn_scaled_lockstep_with_oracle():
     from tests.twin import Twin
     T, L = 16, 2
-    t = Twin(L, 32, 8, 128, T, 420, 300, 256, 72, 640, seed=5)
-    ch = Churn(t, 256, 2048 // 128, 131072 // 128, 2, 32, T, L, seed=5, slab=64, compact_every=16)
+    t = Twin(L, 32, 8, 128, T, 160, 120, 256, 72, 640, seed=5)
+    ch = Churn(t, 256, 2048 // 128, 131072 // 128, 8, 64, T, L, seed=5, slab=64, compact_every=16)
 
     def on_step(c, it):
         if it % 10 == 0:
