@@ -235,6 +235,8 @@ def main():
     lens = np.full(B, wl.context, np.int64)
     n_steps = args.warmup + args.steps
     e2e_steps = 0 if args.no_e2e else args.steps
+    UNFUSED_STEPS = 3  # comparison: separate kv_append + attention launches
+    e2e_steps += UNFUSED_STEPS
     inputs = []
     for s in range(n_steps + e2e_steps):
         inputs.append(W.decode_inputs(wl, s, lens + s))
@@ -245,7 +247,7 @@ def main():
     sp = stream.cuda_stream
     attn_ev, app_ev, reserve_s = [], [], []
 
-    def step(q, k, v, record=False):
+    def step(q, k, v, record=False, fused=True):
         t0 = time.perf_counter()
         rc = pool.reserve(reqs, ones, sp)
         if record:
@@ -253,19 +255,27 @@ def main():
         if rc:
             raise ellm.EllmError(rc, "reserve")
         for l in range(L):
-            if record:
-                a0 = torch.cuda.Event(enable_timing=True)
-                a0.record(stream)
-            rc = pool.append(l, reqs, ones, k[l], v[l], sp)
-            if rc:
-                raise ellm.EllmError(rc, "append")
-            if record:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                app_ev.append((a0, e0))
-            rc = pool.attention(l, reqs, q[l], out[l], scale, sp)
-            if rc:
-                raise ellm.EllmError(rc, "attention")
+            if fused:  # kv_append + attention + split-K merge in one launch per layer
+                if record:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                rc = pool.decode_append_attention(l, reqs, k[l], v[l], q[l], out[l], scale, sp)
+                if rc:
+                    raise ellm.EllmError(rc, "decode_append_attention")
+            else:
+                if record:
+                    a0 = torch.cuda.Event(enable_timing=True)
+                    a0.record(stream)
+                rc = pool.append(l, reqs, ones, k[l], v[l], sp)
+                if rc:
+                    raise ellm.EllmError(rc, "append")
+                if record:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    app_ev.append((a0, e0))
+                rc = pool.attention(l, reqs, q[l], out[l], scale, sp)
+                if rc:
+                    raise ellm.EllmError(rc, "attention")
             if record:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(stream)
@@ -323,14 +333,16 @@ def main():
             traffic = None
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
-            "kernel": "paged_attn_kernel + attn_combine_kernel (one ellm_paged_decode_attention call)",
+            "kernel": ("paged_attn_kernel: one ellm_decode_append_attention launch per layer (new-token "
+                       "K/V append + attention + fused split-K merge)"),
             "alg_bytes_per_launch": int(alg_bytes), "launch_ms": round(attn_mean, 4), "peak_source": peak_src}
 
     # ---- end to end through host buffers: H2D of each step's inputs, D2H of its outputs ----
     e2e = None
-    if e2e_steps:
+    n_e2e = e2e_steps - UNFUSED_STEPS
+    if n_e2e:
         hin = []
-        for s in range(n_steps, n_steps + e2e_steps):
+        for s in range(n_steps, n_steps + n_e2e):
             hin.append(tuple(x.cpu().pin_memory() for x in inputs[s]))
         dq, dk, dv = (torch.empty_like(x) for x in inputs[0])
         hout = torch.empty(out.shape, dtype=out.dtype).pin_memory()
@@ -352,10 +364,20 @@ def main():
             t = torch.tensor([ems], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t[0])
-        e2e = {"value": round(B * e2e_steps / (ems / 1e3), 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ems / e2e_steps, 3)}
+        e2e = {"value": round(B * n_e2e / (ems / 1e3), 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ems / n_e2e, 3)}
 
     swap = measure_swap(pool, wl, stream) if swap_chunks else None
+
+    # ---- unfused comparison: the same step as separate kv_append and attention launches ----
+    barrier()
+    u0, u1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    u0.record(stream)
+    for s in range(n_steps + e2e_steps - UNFUSED_STEPS, n_steps + e2e_steps):
+        step(*inputs[s], record=True, fused=False)
+    u1.record(stream)
+    barrier()
+    unfused_ms = u0.elapsed_time(u1) / UNFUSED_STEPS
 
     # ---- the other §8(a) rows: reserve (a2), append (a3), VMM create / grow / shrink (a1, a9) ----
     app_us = statistics.mean(a.elapsed_time(b) for a, b in app_ev) * 1e3
@@ -376,7 +398,8 @@ def main():
                            "map_us_per_chunk": round(st_create["map_ns"] / max(1, st_create["n_map"]) / 1e3, 2),
                            "mapped_gib": round(st_create["mapped_bytes"] / 2 ** 30, 2)},
         "a2_kv_reserve": {"host_us_per_call": round(statistics.mean(reserve_s) * 1e6, 2), "requests": B},
-        "a3_kv_append": {"decode_us_per_call": round(app_us, 2),
+        "step_fused_vs_unfused_ms": {"fused": round(ms_step, 4), "unfused": round(unfused_ms, 4)},
+        "a3_kv_append": {"decode_us_per_call_unfused": round(app_us, 2),
                          "decode_bytes_per_call": 2 * 2 * B * wl.hkv_local * wl.head_dim * 2,
                          "bulk_gbs": round(bulk_b / bulk_s / 1e9, 1), "bulk_frac": round(bulk_b / bulk_s / 1e9 / peak, 3),
                          "bulk_calls": len(prefill_appends), "bulk_bytes_per_call": int(bulk_b / len(prefill_appends))},

@@ -82,6 +82,10 @@ typedef struct {
   int32_t max_requests;            /* request ids are [0, max_requests) */
   int32_t max_chunks_per_request;  /* table row length (the KV eTensor span) */
   int64_t host_slots;              /* pinned host slots, chunk_bytes each (CPU buffer P_B) */
+  int64_t map_unit_bytes;          /* physical allocation unit backing consecutive chunks: 0 = auto
+                                      (>= 64 MiB; VMM cost is per handle), else a multiple of
+                                      lcm(chunk_bytes, granularity). ellm_alias_request needs
+                                      map_unit_bytes == chunk_bytes. */
 } ellm_pool_config;
 
 typedef struct {
@@ -145,6 +149,15 @@ int ellm_kv_append(ellm_pool* pool, int32_t layer, int32_t n, const int32_t* req
  * RNE). len == 0 -> INVALID_ARG; any chunk of the request in a host slot -> NOT_RESIDENT. */
 int ellm_paged_decode_attention(ellm_pool* pool, int32_t layer, int32_t n, const int32_t* req_ids,
                                 const void* q, void* out, float softmax_scale, void* stream);
+
+/* decode_append_attention (a3 + a4 + a5 fused for decode): exactly kv_append(layer, n, req_ids,
+ * n_new = 1 each, k_new, v_new) followed by paged_decode_attention(layer, n, req_ids, q, out,
+ * softmax_scale), in one kernel launch: the CTA that streams a request's last tile first writes
+ * the new token's K/V rows into the chunk, then reads the tile. Requires distinct requests whose
+ * latest reservation is exactly 1 token (else INVALID_ARG); errors as the two calls. */
+int ellm_decode_append_attention(ellm_pool* pool, int32_t layer, int32_t n, const int32_t* req_ids,
+                                 const void* k_new, const void* v_new, const void* q, void* out,
+                                 float softmax_scale, void* stream);
 
 /* release: all device chunks and host slots of req become FREE; len = 0. */
 int ellm_release(ellm_pool* pool, int32_t req_id, void* stream);

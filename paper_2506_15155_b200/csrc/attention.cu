@@ -116,7 +116,8 @@ struct Params {
   const int32_t* table;
   const int32_t* req;
   const int32_t* len;
-  const int32_t* cum;
+  const int32_t* cum_s;    // [n_vr + 1] prefix of static tiles per virtual request
+  const int32_t* cum_d;    // [n_vr + 1] prefix of dynamic tiles per virtual request
   const int32_t* b_first;  // static owners of vr: CTAs [b_first, b_last] (empty if b_last < b_first)
   const int32_t* b_last;
   const int32_t* u_first;  // dynamic owners of vr: units [u_first, u_last] (empty if u_last < u_first)
@@ -126,9 +127,14 @@ struct Params {
   unsigned long long ticket_base;
   const __nv_bfloat16* q;
   __nv_bfloat16* out;
+  const uint4* k_new;      // fused decode append: [n][Hkv][d] new token rows, or nullptr
+  const uint4* v_new;
+  uint8_t* pool;           // pool VA base (chunk c at pool + c * chunk_bytes)
+  int64_t chunk_bytes;
+  int32_t Hkv;             // local kv-heads (chunk layout [L][2][Hkv][T][d])
   float* part;
   float* part_ml;
-  int64_t W, W_s, U, n_dyn;  // tiles; static tiles; tiles per dynamic unit; dynamic units
+  int64_t W_s, W_d, U, n_dyn;  // static tiles; dynamic tiles; tiles per dynamic unit; units
   int32_t rec_dyn;           // record owner id of dynamic unit 0 (= G + n_vr)
   int32_t table_stride, n_vr, HG, G, T, L, layer, group, Hq;
   float scale_log2;
@@ -138,42 +144,67 @@ constexpr int kFirst = 1, kLast = 2, kDone = 4;  // stage metadata flags
 // LSE merge of the partial records of virtual request vr, run by the 256
 // consumer threads of the last CTA to finish it:
 //   M = max_p m_p,  L = sum_p 2^(m_p - M) l_p,  o = sum_p 2^(m_p - M) o_p / L   -> bf16 (RNE).
-// Records of other SMs are read through L2 (__ldcg): L1 is not coherent across SMs.
+// LPR = D/4 lanes own one q-head row (a float4 of o each): the max and the sum over records
+// are lane-parallel reductions, each record's weight is broadcast by shuffle, and a record's o
+// row is one coalesced D*4-byte load across the row's lanes. Records written by other SMs are
+// read through L2 (__ldcg): L1 is not coherent across SMs.
 template <int D>
 __device__ __forceinline__ void merge_request(const Params& p, int vr, int rows, int nsub, int HB) {
-  // record ranges: static owners (CTAs b) then dynamic owners (units u); record id of
+  constexpr int LPR = D / 4;         // lanes per row
+  constexpr int RPW = 32 / LPR;      // rows per warp pass
+  // record ranges: static owners (CTAs b), then dynamic owners (units u); record id of
   // (owner, vr) is owner + vr, each with nsub subtile slots
   const int64_t s0 = int64_t(__ldg(p.b_first + vr) + vr) * nsub;
-  const int64_t s1 = int64_t(__ldg(p.b_last + vr) + vr + 1) * nsub;
+  const int64_t ns = int64_t(__ldg(p.b_last + vr) - __ldg(p.b_first + vr) + 1) * nsub;
   const int64_t d0 = int64_t(p.rec_dyn + __ldg(p.u_first + vr) + vr) * nsub;
-  const int64_t d1 = int64_t(p.rec_dyn + __ldg(p.u_last + vr) + vr + 1) * nsub;
+  const int64_t nd = int64_t(__ldg(p.u_last + vr) - __ldg(p.u_first + vr) + 1) * nsub;  // 0 if none
+  const int64_t P = ns + nd;
+  auto pid = [&](int64_t k) { return k < ns ? s0 + k : d0 + (k - ns); };
   const int ireq = vr / p.HG, hg = vr % p.HG;
-  for (int item = threadIdx.x; item < rows * (D / 4); item += kConsumerWarps * 32) {
-    const int row = item / (D / 4), e4 = item % (D / 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int e4 = lane % LPR, sub = lane / LPR;
+  const unsigned seg_mask = RPW == 1 ? 0xffffffffu : (0xffffu << (16 * sub));
+  for (int row0 = warp * RPW; row0 < rows; row0 += kConsumerWarps * RPW) {
+    const int row = row0 + sub;
+    const bool live = row < rows;
     float M = -INFINITY;
-    for (int64_t pp = s0; pp < s1; ++pp) M = fmaxf(M, __ldcg(p.part_ml + (pp * rows + row) * 2));
-    for (int64_t pp = d0; pp < d1; ++pp) M = fmaxf(M, __ldcg(p.part_ml + (pp * rows + row) * 2));
+    for (int64_t k = e4; live && k < P; k += LPR) M = fmaxf(M, __ldcg(p.part_ml + (pid(k) * rows + row) * 2));
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(seg_mask, M, o));
     float L = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    auto add = [&](int64_t pp) {
-      const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.part_ml + (pp * rows + row) * 2));
-      const float w = ex2(ml.x - M);  // a record with no valid token has m = -inf -> weight 0
-      const float4 o = __ldcg(reinterpret_cast<const float4*>(p.part + (pp * rows + row) * D) + e4);
-      L += w * ml.y;
-      acc.x += w * o.x;
-      acc.y += w * o.y;
-      acc.z += w * o.z;
-      acc.w += w * o.w;
-    };
-    for (int64_t pp = s0; pp < s1; ++pp) add(pp);
-    for (int64_t pp = d0; pp < d1; ++pp) add(pp);
-    const float inv = 1.f / L;
-    __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
-    __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
-    uint2 v;
-    v.x = *reinterpret_cast<uint32_t*>(&lo);
-    v.y = *reinterpret_cast<uint32_t*>(&hi);
-    *reinterpret_cast<uint2*>(p.out + (int64_t(ireq) * p.Hq + hg * HB * p.group + row) * D + 4 * e4) = v;
+    for (int64_t base = 0; base < P; base += LPR) {
+      float my_w = 0.f;
+      const int64_t mk = base + e4;
+      if (live && mk < P) {
+        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.part_ml + (pid(mk) * rows + row) * 2));
+        my_w = ex2(ml.x - M);  // a record with no valid token has m = -inf -> weight 0
+        L += my_w * ml.y;
+      }
+      const int cnt = int(min(int64_t(LPR), P - base));
+#pragma unroll 4
+      for (int j = 0; j < cnt; ++j) {
+        const float w = __shfl_sync(seg_mask, my_w, j, LPR);
+        if (live) {
+          const float4 o = __ldcg(reinterpret_cast<const float4*>(p.part + (pid(base + j) * rows + row) * D) + e4);
+          acc.x += w * o.x;
+          acc.y += w * o.y;
+          acc.z += w * o.z;
+          acc.w += w * o.w;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) L += __shfl_xor_sync(seg_mask, L, o);
+    if (live) {
+      const float inv = 1.f / L;
+      __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+      uint2 v;
+      v.x = *reinterpret_cast<uint32_t*>(&lo);
+      v.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(p.out + (int64_t(ireq) * p.Hq + hg * HB * p.group + row) * D + 4 * e4) = v;
+    }
   }
 }
 
@@ -230,23 +261,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
     int stage = 0;
     uint32_t phase = 0;
-    // Ranges of the flat tile space this CTA streams: first its static share of the first W_s
-    // tiles, then dynamic U-tile units claimed from a ticket counter (the next ticket is
-    // requested before the current unit is streamed, hiding the atomic's latency). `owner`
-    // names the partial records a range produces: record of (owner, vr) = owner + vr, unique
-    // along the monotone staircase of (owner, request) pairs.
+    // Two tile spaces: the static space holds the first stat(vr) tiles of every request
+    // (prefix cum_s), the dynamic space its last dyn(vr) tiles (prefix cum_d). This CTA streams
+    // its balanced share of the static space, then dynamic U-tile units claimed from a ticket
+    // counter (the next ticket is requested before the current unit is streamed, hiding the
+    // atomic's latency). `owner` names the partial records a range produces: record of
+    // (owner, vr) = owner + vr, unique along the monotone staircase of (owner, request) pairs.
     int64_t t_begin = int64_t(b) * p.W_s / p.G, t_end = int64_t(b + 1) * p.W_s / p.G;
     int owner = b;
+    const int32_t* cum = p.cum_s;
     unsigned long long next_ticket = 0;
     if (p.n_dyn > 0 && lane == 0) next_ticket = atomicAdd(p.ticket, 1ull);
     for (;;) {
-      int vr = find_vr(p.cum, p.n_vr, t_begin);
+      int vr = find_vr(cum, p.n_vr, t_begin);
       for (int64_t tile = t_begin; tile < t_end; ++vr) {
-        const int64_t seg_end = min(t_end, int64_t(__ldg(p.cum + vr + 1)));
+        const int64_t seg_end = min(t_end, int64_t(__ldg(cum + vr + 1)));
         const int ireq = vr / p.HG, hg = vr % p.HG;
         const int32_t len = __ldg(p.len + ireq);
         const int32_t* trow = p.table + int64_t(__ldg(p.req + ireq)) * p.table_stride;
-        const int64_t tile0 = __ldg(p.cum + vr);
+        // space coordinate of the request's first tile in this space, minus its tile offset
+        const int64_t tile0 = __ldg(cum + vr) -
+                              (cum == p.cum_d ? int64_t(__ldg(p.cum_s + vr + 1) - __ldg(p.cum_s + vr)) : 0);
         {  // warm L1 with this segment's Q rows for the consumers (they read them at FIRST)
           const char* qb = reinterpret_cast<const char*>(p.q + (int64_t(ireq) * p.Hq + hg * HB * p.group) * D);
           for (int off = lane * 128; off < HB * p.group * D * 2; off += 32 * 128)
@@ -268,6 +303,29 @@ __global__ void __launch_bounds__(kThreads, 1)
             int32_t e[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) e[k] = __shfl_sync(0xffffffffu, ent[k], u);
+            if (p.k_new != nullptr && (t + u - tile0 + 1) * TT >= len) {
+              // fused decode append: this is the request's last tile, which holds position
+              // len-1; write the new K/V rows of heads [hg*HB, hg*HB+HB) into the chunk, then
+              // order these generic-proxy stores before the tile's TMA (async proxy) read.
+              const int32_t pos = len - 1;
+              const int kp = int((pos - (t + u - tile0) * TT) / tok_box);  // piece holding pos
+              int32_t c = e[0];
+#pragma unroll
+              for (int k = 1; k < 8; ++k)
+                if (k == kp) c = e[k];  // select, not a dynamic index (keeps e[] in registers)
+              constexpr int PARTS = D / 8, UNITS = 2 * HB * PARTS;
+              for (int w = lane; w < UNITS; w += 32) {
+                const int kv = w / (HB * PARTS), h = (w / PARTS) % HB, part = w % PARTS;
+                const uint4* src = kv ? p.v_new : p.k_new;
+                const uint4 val = __ldg(src + (int64_t(ireq) * p.Hkv + hg * HB + h) * PARTS + part);
+                uint8_t* dst = p.pool + int64_t(c) * p.chunk_bytes +
+                               ((int64_t(p.layer * 2 + kv) * p.Hkv + hg * HB + h) * p.T + pos % p.T) * (D * 2) +
+                               part * 16;
+                *reinterpret_cast<uint4*>(dst) = val;
+              }
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+              __syncwarp();
+            }
             if (lane == 0) {
               mbar_wait(empty0 + 8 * stage, phase ^ 1);
               const int64_t tl = t + u;
@@ -296,9 +354,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t u = int64_t(__shfl_sync(0xffffffffu, next_ticket, 0) - p.ticket_base);
       if (u >= p.n_dyn) break;
       if (lane == 0) next_ticket = atomicAdd(p.ticket, 1ull);
-      t_begin = p.W_s + u * p.U;
-      t_end = min(p.W, t_begin + p.U);
+      t_begin = u * p.U;
+      t_end = min(p.W_d, t_begin + p.U);
       owner = p.rec_dyn + int(u);
+      cum = p.cum_d;
     }
     // no more work: publish DONE through the next stage (plain arrive, no bytes)
     if (lane == 0) {
@@ -538,7 +597,8 @@ cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh,
   prm.table = table;
   prm.req = d.req;
   prm.len = d.len;
-  prm.cum = d.cum;
+  prm.cum_s = d.cum_s;
+  prm.cum_d = d.cum_d;
   prm.b_first = d.b_first;
   prm.b_last = d.b_last;
   prm.u_first = d.u_first;
@@ -548,10 +608,15 @@ cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh,
   prm.ticket_base = plan.ticket_base;
   prm.q = static_cast<const __nv_bfloat16*>(q);
   prm.out = static_cast<__nv_bfloat16*>(out);
+  prm.k_new = static_cast<const uint4*>(plan.k_new);
+  prm.v_new = static_cast<const uint4*>(plan.v_new);
+  prm.pool = plan.pool;
+  prm.chunk_bytes = plan.chunk_bytes;
+  prm.Hkv = sh.Hkv;
   prm.part = part;
   prm.part_ml = part_ml;
-  prm.W = plan.W;
   prm.W_s = plan.W_s;
+  prm.W_d = plan.W_d;
   prm.U = plan.U;
   prm.n_dyn = plan.n_dyn;
   prm.rec_dyn = G + n_vr;

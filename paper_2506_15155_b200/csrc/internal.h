@@ -97,19 +97,26 @@ cudaError_t launch_chunk_copy(uint8_t* dst_base, const int32_t* dst_idx, const u
 struct AttnDesc {  // device-resident
   const int32_t* req;      // [n]
   const int32_t* len;      // [n]
-  const int32_t* cum;      // [n_vr + 1] tiles
+  const int32_t* cum_s;    // [n_vr + 1] prefix of static tiles (first stat(vr) tiles of vr)
+  const int32_t* cum_d;    // [n_vr + 1] prefix of dynamic tiles (last dyn(vr) tiles of vr)
   const int32_t* b_first;  // [n_vr] static owner CTAs of vr (empty if last < first)
   const int32_t* b_last;   // [n_vr]
   const int32_t* u_first;  // [n_vr] dynamic owner units of vr (empty if last < first)
   const int32_t* u_last;   // [n_vr]
 };
-// Schedule of one attention launch over W stage-tiles: the first W_s are split statically over
-// G CTAs, the rest in n_dyn units of U tiles claimed with a ticket counter.
+// Schedule of one attention launch: the W_s static tiles (the first stat(vr) tiles of every
+// request) are split evenly over G CTAs; the W_d dynamic tiles (the last dyn(vr) = tiles(vr) /
+// dyn_div of every request) go in n_dyn units of U tiles claimed with a ticket counter.
 struct AttnPlan {
-  int64_t W = 0, W_s = 0, U = 1, n_dyn = 0;
+  int64_t W_s = 0, W_d = 0, U = 1, n_dyn = 0;
   int32_t G = 0;
   unsigned long long* ticket = nullptr;
   unsigned long long ticket_base = 0;
+  // fused decode append (ellm_decode_append_attention): one new token per request, or nullptr
+  const void* k_new = nullptr;
+  const void* v_new = nullptr;
+  uint8_t* pool = nullptr;
+  int64_t chunk_bytes = 0;
 };
 struct AttnShape {
   int32_t D, HB, HG, Hkv, Hq, group, T, L, TT, nsub;
@@ -185,6 +192,8 @@ struct ellm_pool {
   ellm::AttnPlan cache_plan;
   unsigned long long* d_ticket = nullptr;  // dynamic-unit ticket counter (device)
   uint64_t ticket_base = 0;                // tickets consumed by earlier launches
+  int64_t dyn_div = 8;                     // dynamic tail = W / dyn_div tiles (0: static only)
+  int64_t dyn_unit = 8;                    // minimum tiles per dynamic unit
 
   std::map<int32_t, std::pair<CUdeviceptr, size_t>> alias;
   int last_cuda_error = 0;

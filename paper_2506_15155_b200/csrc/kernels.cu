@@ -17,36 +17,51 @@ __global__ void table_scatter_kernel(int32_t* __restrict__ table, const TableUpd
   }
 }
 
-// One 16-byte unit per thread iteration. Unit u covers K (u < half) or V; within a half the
-// order is (row, head, part) so reads of k_new / v_new are fully coalesced, and the 16 B
-// parts of one (row, head) land contiguously in its slab row (layout [L][2][Hkv][T][d]).
+// One warp per new token row: the request / position / chunk of the row are resolved once
+// (binary search over cum_rows, one table read), then the row's K and V (Hkv*d*2 bytes each,
+// contiguous in k_new / v_new) move as 16-byte units, all loads in flight before the stores.
+// Each (kv, head) lands as one contiguous d*2-byte row of its slab (layout [L][2][Hkv][T][d]).
+constexpr int kAppendMaxPerLane = 8;  // 16-byte units per lane per kv: Hkv*d/8 <= 256
 __global__ void __launch_bounds__(256) kv_append_kernel(
     const int32_t* __restrict__ req, const int32_t* __restrict__ pos0,
-    const int32_t* __restrict__ cum_rows, int32_t n, int64_t half_units, const int32_t* __restrict__ table,
+    const int32_t* __restrict__ cum_rows, int32_t n, int64_t total_rows, const int32_t* __restrict__ table,
     int32_t table_stride, uint8_t* __restrict__ pool, int64_t chunk_bytes, int32_t T, int32_t layer,
     int32_t Hkv, int32_t parts, const uint4* __restrict__ k_new, const uint4* __restrict__ v_new) {
-  const int64_t total = 2 * half_units;
-  for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < total;
-       u += int64_t(gridDim.x) * blockDim.x) {
-    const int kv = u >= half_units;
-    const int64_t w = kv ? u - half_units : u;
-    const uint4 val = kv ? __ldg(v_new + w) : __ldg(k_new + w);
-    const int32_t part = int32_t(w % parts);
-    const int64_t rh = w / parts;
-    const int32_t h = int32_t(rh % Hkv);
-    const int32_t row = int32_t(rh / Hkv);
-    // request of this row: largest i with cum_rows[i] <= row
-    int lo = 0, hi = n - 1;
+  const int lane = threadIdx.x & 31;
+  const int units = Hkv * parts;  // 16-byte units per row and kv
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t row = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); row < total_rows;
+       row += warps) {
+    int lo = 0, hi = n - 1;  // request of this row: largest i with cum_rows[i] <= row
     while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
+      const int mid = (lo + hi + 1) >> 1;
       if (__ldg(cum_rows + mid) <= row) lo = mid; else hi = mid - 1;
     }
-    const int32_t p = __ldg(pos0 + lo) + (row - __ldg(cum_rows + lo));
+    const int32_t p = __ldg(pos0 + lo) + int32_t(row - __ldg(cum_rows + lo));
     const int32_t c = __ldg(table + int64_t(__ldg(req + lo)) * table_stride + p / T);
-    const int64_t off = int64_t(c) * chunk_bytes +
-                        ((int64_t(layer * 2 + kv) * Hkv + h) * T + (p % T)) * int64_t(parts) * 16 +
-                        int64_t(part) * 16;
-    *reinterpret_cast<uint4*>(pool + off) = val;
+    uint8_t* kdst = pool + int64_t(c) * chunk_bytes + (int64_t(layer * 2) * Hkv * T + (p % T)) * parts * 16;
+    uint8_t* vdst = kdst + int64_t(Hkv) * T * parts * 16;
+    const uint4* ksrc = k_new + row * units;
+    const uint4* vsrc = v_new + row * units;
+    uint4 kv_[2 * kAppendMaxPerLane];
+#pragma unroll
+    for (int i = 0; i < kAppendMaxPerLane; ++i) {
+      const int u = lane + 32 * i;
+      if (u < units) {
+        kv_[i] = __ldg(ksrc + u);
+        kv_[kAppendMaxPerLane + i] = __ldg(vsrc + u);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kAppendMaxPerLane; ++i) {
+      const int u = lane + 32 * i;
+      if (u < units) {
+        const int h = u / parts, part = u - h * parts;
+        const int64_t off = (int64_t(h) * T * parts + part) * 16;
+        *reinterpret_cast<uint4*>(kdst + off) = kv_[i];
+        *reinterpret_cast<uint4*>(vdst + off) = kv_[kAppendMaxPerLane + i];
+      }
+    }
   }
 }
 
@@ -90,10 +105,10 @@ cudaError_t launch_kv_append(const AppendDesc& d, int32_t n, int64_t total_rows,
                              int32_t layer, int32_t Hkv, int32_t D, const void* k_new,
                              const void* v_new, int num_sms, cudaStream_t s) {
   const int32_t parts = D / 8;
-  const int64_t half_units = total_rows * Hkv * parts;
-  int64_t blocks = (2 * half_units + 255) / 256;
+  if (Hkv * parts > 32 * kAppendMaxPerLane) return cudaErrorInvalidValue;
+  const int64_t blocks = (total_rows + 7) / 8;  // 8 warps (rows) per block
   int grid = int(std::min<int64_t>(blocks, int64_t(num_sms) * 8));
-  kv_append_kernel<<<grid, 256, 0, s>>>(d.req, d.pos0, d.cum_rows, n, half_units, table, table_stride,
+  kv_append_kernel<<<grid, 256, 0, s>>>(d.req, d.pos0, d.cum_rows, n, total_rows, table, table_stride,
                                         pool, chunk_bytes, T, layer, Hkv, parts,
                                         static_cast<const uint4*>(k_new), static_cast<const uint4*>(v_new));
   return cudaGetLastError();

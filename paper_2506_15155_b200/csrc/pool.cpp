@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <set>
 
 #include "internal.h"
@@ -122,11 +123,6 @@ int upload_ints(ellm_pool* p, const std::vector<int32_t>& v, cudaStream_t stream
   return ELLM_OK;
 }
 
-int map_unit_if_needed(ellm_pool* p, int64_t unit) {
-  if (!p->has_dev || p->vt->mapped[size_t(unit)]) return ELLM_OK;
-  return ellm_vtensor_map(p->vt, unit, 1);
-}
-
 bool check_reqs_range(const ellm_pool* p, int32_t n, const int32_t* r) {
   for (int32_t i = 0; i < n; ++i)
     if (r[i] < 0 || r[i] >= p->cfg.max_requests) return false;
@@ -181,6 +177,9 @@ int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out) {
   p->group = group;
   p->chunk_bytes = int64_t(4) * T * c.n_layers * c.n_heads_kv * c.head_dim;
   p->has_dev = c.device != ELLM_DEVICE_NONE;
+  // schedule tuning knobs (defaults documented in DESIGN.md §5)
+  if (const char* v = std::getenv("ELLM_ATTN_DYN_DIV")) p->dyn_div = std::max(0L, std::atol(v));
+  if (const char* v = std::getenv("ELLM_ATTN_DYN_UNIT")) p->dyn_unit = std::max(1L, std::atol(v));
   p->owner.assign(size_t(c.max_chunks), ACT);
   p->used.assign(size_t(c.max_chunks), 0);
   for (int64_t i = 0; i < c.initial_chunks; ++i) p->owner[size_t(i)] = KV;
@@ -210,21 +209,32 @@ int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out) {
   size_t gran = 0;
   int rc = ellm_vmm_granularity(c.device, &gran);
   if (rc) return fail(rc);
-  if (p->chunk_bytes % int64_t(gran) == 0) {
-    p->unit_bytes = p->chunk_bytes;
-    p->chunks_per_unit = 1;
-  } else if (int64_t(gran) % p->chunk_bytes == 0) {
-    p->unit_bytes = int64_t(gran);
-    p->chunks_per_unit = int64_t(gran) / p->chunk_bytes;
+  // Physical map unit: a multiple of lcm(chunk_bytes, granularity). Driver VMM cost on B200 is
+  // per handle (cuMemCreate ~0.1 ms, cuMemSetAccess ~0.2-1 ms per handle, measured), so the
+  // default unit is >= 64 MiB; KV/ACT ownership stays per chunk and a unit's memory is released
+  // once all of its chunks are ACT (R1, §5).
+  const int64_t g64 = int64_t(gran);
+  int64_t lcm = p->chunk_bytes;
+  while (lcm % g64 != 0) lcm += p->chunk_bytes;
+  if (c.map_unit_bytes > 0) {
+    if (c.map_unit_bytes % lcm != 0) return fail(ELLM_ERR_UNSUPPORTED);
+    p->unit_bytes = c.map_unit_bytes;
   } else {
-    return fail(ELLM_ERR_UNSUPPORTED);
+    p->unit_bytes = lcm * ((int64_t(64) << 20) + lcm - 1) / lcm;
+    const int64_t pool_bytes = ((c.max_chunks * p->chunk_bytes + lcm - 1) / lcm) * lcm;
+    p->unit_bytes = std::min(p->unit_bytes, pool_bytes);
   }
+  p->chunks_per_unit = p->unit_bytes / p->chunk_bytes;
   int64_t n_units = (c.max_chunks + p->chunks_per_unit - 1) / p->chunks_per_unit;
   if ((rc = ellm_vtensor_create(c.device, size_t(p->unit_bytes), n_units, &p->vt))) return fail(rc);
   p->unit_kv.assign(size_t(n_units), 0);
   for (int64_t i = 0; i < c.initial_chunks; ++i) ++p->unit_kv[size_t(i / p->chunks_per_unit)];
-  for (int64_t u = 0; u < n_units; ++u)
-    if (p->unit_kv[size_t(u)] > 0 && (rc = ellm_vtensor_map(p->vt, u, 1))) return fail(rc);
+  for (int64_t u = 0; u < n_units;) {  // map runs of units that hold KV chunks
+    int64_t v = u;
+    while (v < n_units && p->unit_kv[size_t(v)] > 0) ++v;
+    if (v > u && (rc = ellm_vtensor_map(p->vt, u, v - u))) return fail(rc);
+    u = v + 1;
+  }
   if (c.host_slots > 0) {
     if ((e = cudaHostAlloc(reinterpret_cast<void**>(&p->host_slots),
                            size_t(c.host_slots) * size_t(p->chunk_bytes),
@@ -402,6 +412,9 @@ int ellm_kv_append(ellm_pool* p, int32_t layer, int32_t n, const int32_t* reqs,
 }
 
 // a4 + a5 — O4: exact softmax attention over the accumulated KV.
+static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t* reqs, const void* q,
+                          void* out, float scale, void* stream, const void* k_new, const void* v_new);
+
 int ellm_paged_decode_attention(ellm_pool* p, int32_t layer, int32_t n, const int32_t* reqs,
                                 const void* q, void* out, float scale, void* stream) {
   if (!p || n < 0 || (n > 0 && !reqs)) return ELLM_ERR_INVALID_ARG;
@@ -413,6 +426,31 @@ int ellm_paged_decode_attention(ellm_pool* p, int32_t layer, int32_t n, const in
     if (p->nonres[size_t(reqs[i])] > 0) return ELLM_ERR_NOT_RESIDENT;
   if (!p->has_dev) return ELLM_ERR_NO_DEVICE;
   if (n == 0) return ELLM_OK;
+  return attention_impl(p, layer, n, reqs, q, out, scale, stream, nullptr, nullptr);
+}
+
+// a3 + a4 + a5 fused for decode: kv_append of one token per request, then attention.
+int ellm_decode_append_attention(ellm_pool* p, int32_t layer, int32_t n, const int32_t* reqs,
+                                 const void* k_new, const void* v_new, const void* q, void* out,
+                                 float scale, void* stream) {
+  if (!p || n < 0 || (n > 0 && !reqs)) return ELLM_ERR_INVALID_ARG;
+  if (layer < 0 || layer >= p->cfg.n_layers) return ELLM_ERR_OUT_OF_RANGE;
+  if (!check_reqs_range(p, n, reqs)) return ELLM_ERR_OUT_OF_RANGE;
+  if (has_dup(n, reqs)) return ELLM_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (p->pending[size_t(reqs[i])] != 1) return ELLM_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (p->nonres[size_t(reqs[i])] > 0) return ELLM_ERR_NOT_RESIDENT;
+  if (!p->has_dev) return ELLM_ERR_NO_DEVICE;
+  if (n == 0) return ELLM_OK;
+  if (!k_new || !v_new) return ELLM_ERR_INVALID_ARG;
+  return attention_impl(p, layer, n, reqs, q, out, scale, stream, k_new, v_new);
+}
+
+}  // extern "C"
+
+static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t* reqs, const void* q,
+                          void* out, float scale, void* stream, const void* k_new, const void* v_new) {
   if (!q || !out || !std::isfinite(scale)) return ELLM_ERR_INVALID_ARG;
   const AttnShape& a = p->ash;
   const int32_t n_vr = n * a.HG;
@@ -423,56 +461,54 @@ int ellm_paged_decode_attention(ellm_pool* p, int32_t layer, int32_t n, const in
     key[size_t(n + i)] = int32_t(p->len[size_t(reqs[i])]);
   }
   if (key != p->cache_key || !p->ring.still_valid(p->cache_dev, p->cache_gen)) {
-    // layout: req[n] len[n] cum[n_vr+1] b_first[n_vr] b_last[n_vr] u_first[n_vr] u_last[n_vr]
-    std::vector<int32_t> d(size_t(2 * n + 5 * n_vr + 1));
-    int64_t W = 0;
+    // layout: req[n] len[n] cum_s[n_vr+1] cum_d[n_vr+1] b_first[n_vr] b_last[n_vr]
+    //         u_first[n_vr] u_last[n_vr]
+    std::vector<int32_t> d(size_t(2 * n + 6 * n_vr + 2));
     for (int32_t i = 0; i < n; ++i) {
       d[size_t(i)] = reqs[i];
       d[size_t(n + i)] = key[size_t(n + i)];
     }
-    int32_t* cum = d.data() + 2 * n;
-    for (int32_t vr = 0; vr < n_vr; ++vr) {
-      cum[vr] = int32_t(W);
-      W += (p->len[size_t(reqs[vr / a.HG])] + a.TT - 1) / a.TT;
-    }
-    cum[n_vr] = int32_t(W);
+    int32_t* cum_s = d.data() + 2 * n;
+    int32_t* cum_d = cum_s + n_vr + 1;
+    int64_t W = 0;
+    for (int32_t vr = 0; vr < n_vr; ++vr) W += (p->len[size_t(reqs[vr / a.HG])] + a.TT - 1) / a.TT;
     if (W > INT32_MAX / 2) return ELLM_ERR_UNSUPPORTED;
-    AttnPlan& pl = p->cache_plan;
-    pl.W = W;
-    if (W >= 4 * int64_t(p->num_sms)) {
-      // static share: 7/8 of the tiles, balanced over one CTA per SM; dynamic tail: the rest in
-      // units of >= 8 tiles claimed by whichever CTA is free first (absorbs the per-SM spread)
-      pl.G = p->num_sms;
-      pl.W_s = W - W / 8;
-      pl.U = std::max<int64_t>(8, (W - pl.W_s + kMaxDynUnits - 1) / kMaxDynUnits);
-      pl.n_dyn = (W - pl.W_s + pl.U - 1) / pl.U;
-    } else {
-      // small batch: G = min(#SMs, W) static CTAs, every one owning >= 1 tile
-      pl.G = int32_t(std::min<int64_t>(p->num_sms, W));
-      pl.W_s = W;
-      pl.U = 1;
-      pl.n_dyn = 0;
+    // Dynamic tail only when there is enough work to balance: the last tiles(vr) / dyn_div
+    // tiles of every request go to the dynamic space.
+    const int64_t div = (p->dyn_div > 0 && W >= 4 * int64_t(p->num_sms)) ? p->dyn_div : 0;
+    int64_t Ws = 0, Wd = 0;
+    for (int32_t vr = 0; vr < n_vr; ++vr) {
+      const int64_t tiles = (p->len[size_t(reqs[vr / a.HG])] + a.TT - 1) / a.TT;
+      const int64_t dyn = div ? tiles / div : 0;  // < tiles: every request keeps >= 1 static tile
+      cum_s[vr] = int32_t(Ws);
+      cum_d[vr] = int32_t(Wd);
+      Ws += tiles - dyn;
+      Wd += dyn;
     }
-    // Static CTA b owns tiles [floor(b W_s / G), floor((b+1) W_s / G)); the CTA holding tile t is
-    // floor(((t+1) G - 1) / W_s). Dynamic unit u owns [W_s + u U, W_s + (u+1) U).
-    const int64_t G = pl.G, Ws = pl.W_s;
+    cum_s[n_vr] = int32_t(Ws);
+    cum_d[n_vr] = int32_t(Wd);
+    AttnPlan& pl = p->cache_plan;
+    pl.W_s = Ws;
+    pl.W_d = Wd;
+    // G = min(#SMs, W_s): every static CTA owns >= 1 tile, so every CTA in [b_first, b_last]
+    // writes a record for vr (the merge reads exactly those).
+    pl.G = int32_t(std::min<int64_t>(p->num_sms, Ws));
+    pl.U = Wd ? std::max<int64_t>(p->dyn_unit, (Wd + kMaxDynUnits - 1) / kMaxDynUnits) : 1;
+    pl.n_dyn = Wd ? (Wd + pl.U - 1) / pl.U : 0;
+    // Static CTA b owns [floor(b W_s / G), floor((b+1) W_s / G)) of the static space; the CTA
+    // holding tile t is floor(((t+1) G - 1) / W_s). Dynamic unit u owns [u U, (u+1) U).
+    const int64_t G = pl.G;
     auto cta_of = [&](int64_t t) { return int32_t(((t + 1) * G - 1) / Ws); };
-    int32_t* bf = d.data() + 2 * n + n_vr + 1;
+    int32_t* bf = cum_d + n_vr + 1;
     int32_t* bl = bf + n_vr;
     int32_t* uf = bl + n_vr;
     int32_t* ul = uf + n_vr;
     for (int32_t vr = 0; vr < n_vr; ++vr) {
-      const int64_t t0 = cum[vr], t1 = cum[vr + 1];  // [t0, t1)
-      if (t0 < Ws) {
-        bf[vr] = cta_of(t0);
-        bl[vr] = cta_of(std::min(t1, Ws) - 1);
-      } else {
-        bf[vr] = 0;
-        bl[vr] = -1;
-      }
-      if (t1 > Ws) {
-        uf[vr] = int32_t((std::max(t0, Ws) - Ws) / pl.U);
-        ul[vr] = int32_t((t1 - 1 - Ws) / pl.U);
+      bf[vr] = cta_of(cum_s[vr]);
+      bl[vr] = cta_of(int64_t(cum_s[vr + 1]) - 1);
+      if (cum_d[vr + 1] > cum_d[vr]) {
+        uf[vr] = int32_t(cum_d[vr] / pl.U);
+        ul[vr] = int32_t((int64_t(cum_d[vr + 1]) - 1) / pl.U);
       } else {
         uf[vr] = 0;
         ul[vr] = -1;
@@ -490,11 +526,16 @@ int ellm_paged_decode_attention(ellm_pool* p, int32_t layer, int32_t n, const in
     p->ring.touch(p->cache_dev);
   }
   const int32_t* dd = p->cache_dev;
-  AttnDesc ad{dd, dd + n, dd + 2 * n, dd + 2 * n + n_vr + 1, dd + 2 * n + 2 * n_vr + 1,
-              dd + 2 * n + 3 * n_vr + 1, dd + 2 * n + 4 * n_vr + 1};
+  const int32_t* cs = dd + 2 * n;
+  AttnDesc ad{dd, dd + n, cs, cs + n_vr + 1, cs + 2 * n_vr + 2, cs + 3 * n_vr + 2, cs + 4 * n_vr + 2,
+              cs + 5 * n_vr + 2};
   AttnPlan plan = p->cache_plan;
   plan.ticket = p->d_ticket;
   plan.ticket_base = p->ticket_base;
+  plan.k_new = k_new;
+  plan.v_new = v_new;
+  plan.pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
+  plan.chunk_bytes = p->chunk_bytes;
   int launches = 0;
   cudaError_t e = launch_paged_attention(p->tmap, a, ad, n, n_vr, plan, p->d_table,
                                          p->cfg.max_chunks_per_request, layer, q, out, p->d_part,
@@ -504,6 +545,8 @@ int ellm_paged_decode_attention(ellm_pool* p, int32_t layer, int32_t n, const in
   if (plan.n_dyn > 0) p->ticket_base += uint64_t(plan.n_dyn) + uint64_t(plan.G);  // tickets consumed
   return p->ring.commit(S(stream));
 }
+
+extern "C" {
 
 // O8 — released slots return to the pool.
 int ellm_release(ellm_pool* p, int32_t r, void* stream) {
@@ -671,9 +714,12 @@ int ellm_pool_grow(ellm_pool* p, int64_t n) {
     if (p->owner[size_t(c)] == ACT) ids.push_back(c);
   if (p->has_dev) {  // map first so a driver failure leaves ownership unchanged
     std::set<int64_t> units;
-    for (int64_t c : ids) units.insert(c / p->chunks_per_unit);
-    for (int64_t u : units) {
-      int rc = map_unit_if_needed(p, u);
+    for (int64_t c : ids)
+      if (!p->vt->mapped[size_t(c / p->chunks_per_unit)]) units.insert(c / p->chunks_per_unit);
+    for (auto it = units.begin(); it != units.end();) {  // map contiguous runs at once
+      int64_t u0 = *it, u1 = u0 + 1;
+      for (++it; it != units.end() && *it == u1; ++it) ++u1;
+      int rc = ellm_vtensor_map(p->vt, u0, u1 - u0);
       if (rc) return rc;
     }
   }
@@ -703,11 +749,16 @@ int ellm_pool_shrink(ellm_pool* p, int64_t n) {
       int64_t u = c / p->chunks_per_unit;
       if (p->has_dev && --p->unit_kv[size_t(u)] == 0) units.push_back(u);
     }
-  if (p->has_dev)
-    for (int64_t u : units) {
-      int rc = ellm_vtensor_unmap(p->vt, u, 1);
+  if (p->has_dev) {  // unmap contiguous runs at once (one device sync per run)
+    std::sort(units.begin(), units.end());
+    for (size_t i = 0; i < units.size();) {
+      size_t k = i + 1;
+      while (k < units.size() && units[k] == units[k - 1] + 1) ++k;
+      int rc = ellm_vtensor_unmap(p->vt, units[i], int64_t(k - i));
       if (rc) return rc;
+      i = k;
     }
+  }
   return ELLM_OK;
 }
 

@@ -215,23 +215,35 @@ int ellm_vtensor_map(ellm_vtensor* vt, int64_t first, int64_t n) {
   acc.location.id = vt->device;
   acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
   int64_t t0 = now_ns();
+  auto undo = [&](int64_t upto) {  // roll back slots [first, upto) on a driver failure
+    for (int64_t i = first; i < upto; ++i) {
+      d.memUnmap(vt->base + CUdeviceptr(i) * vt->slot_bytes, vt->slot_bytes);
+      d.memRelease(vt->handles[size_t(i)]);
+      vt->handles[size_t(i)] = 0;
+    }
+  };
   for (int64_t i = first; i < first + n; ++i) {
     CUmemGenericAllocationHandle h;
     CUdeviceptr va = vt->base + CUdeviceptr(i) * vt->slot_bytes;
-    if (d.memCreate(&h, vt->slot_bytes, &p, 0) != CUDA_SUCCESS) return ELLM_ERR_CUDA;
-    if (d.memMap(va, vt->slot_bytes, 0, h, 0) != CUDA_SUCCESS) {
-      d.memRelease(h);
+    if (d.memCreate(&h, vt->slot_bytes, &p, 0) != CUDA_SUCCESS) {
+      undo(i);
       return ELLM_ERR_CUDA;
     }
-    if (d.memSetAccess(va, vt->slot_bytes, &acc, 1) != CUDA_SUCCESS) {
-      d.memUnmap(va, vt->slot_bytes);
+    if (d.memMap(va, vt->slot_bytes, 0, h, 0) != CUDA_SUCCESS) {
       d.memRelease(h);
+      undo(i);
       return ELLM_ERR_CUDA;
     }
     vt->handles[size_t(i)] = h;
-    vt->mapped[size_t(i)] = 1;
-    ++vt->n_map;
   }
+  // one access grant for the whole contiguous run (cuMemSetAccess is required after mapping)
+  if (n > 0 && d.memSetAccess(vt->base + CUdeviceptr(first) * vt->slot_bytes, vt->slot_bytes * size_t(n),
+                              &acc, 1) != CUDA_SUCCESS) {
+    undo(first + n);
+    return ELLM_ERR_CUDA;
+  }
+  for (int64_t i = first; i < first + n; ++i) vt->mapped[size_t(i)] = 1;
+  vt->n_map += n;
   vt->map_ns += now_ns() - t0;
   return ELLM_OK;
 }

@@ -36,7 +36,8 @@ class ellm_pool_config(ctypes.Structure):
                 ("n_heads_kv", ctypes.c_int32), ("head_dim", ctypes.c_int32),
                 ("tokens_per_chunk", ctypes.c_int32), ("max_chunks", ctypes.c_int64),
                 ("initial_chunks", ctypes.c_int64), ("max_requests", ctypes.c_int32),
-                ("max_chunks_per_request", ctypes.c_int32), ("host_slots", ctypes.c_int64)]
+                ("max_chunks_per_request", ctypes.c_int32), ("host_slots", ctypes.c_int64),
+                ("map_unit_bytes", ctypes.c_int64)]
 
 
 class ellm_stats(ctypes.Structure):
@@ -62,6 +63,7 @@ _SIGS = {
     "ellm_kv_reserve": (ctypes.c_int, [_P, _I32, _P, _P, _V]),
     "ellm_kv_append": (ctypes.c_int, [_P, _I32, _I32, _P, _P, _V, _V, _V]),
     "ellm_paged_decode_attention": (ctypes.c_int, [_P, _I32, _I32, _P, _V, _V, ctypes.c_float, _V]),
+    "ellm_decode_append_attention": (ctypes.c_int, [_P, _I32, _I32, _P, _V, _V, _V, _V, ctypes.c_float, _V]),
     "ellm_release": (ctypes.c_int, [_P, _I32, _V]),
     "ellm_deflate": (ctypes.c_int, [_P, _I32, _P, _P, _V]),
     "ellm_inflate": (ctypes.c_int, [_P, _I32, _P, _P, _V]),
@@ -119,10 +121,10 @@ class Pool:
 
     def __init__(self, device: int, n_layers: int, n_heads_q: int, n_heads_kv: int, head_dim: int,
                  tokens_per_chunk: int, max_chunks: int, initial_chunks: int, max_requests: int,
-                 max_chunks_per_request: int, host_slots: int = 0):
+                 max_chunks_per_request: int, host_slots: int = 0, map_unit_bytes: int = 0):
         self.cfg = ellm_pool_config(device, n_layers, n_heads_q, n_heads_kv, head_dim, tokens_per_chunk,
                                     max_chunks, initial_chunks, max_requests, max_chunks_per_request,
-                                    host_slots)
+                                    host_slots, map_unit_bytes)
         h = _P()
         rc = ellm_pool_create(ctypes.byref(self.cfg), ctypes.byref(h))
         if rc != OK:
@@ -168,6 +170,12 @@ class Pool:
         r = _i32(reqs)
         return ellm_paged_decode_attention(self._h, layer, len(r), _ptr(r), _dptr(q), _dptr(out),
                                            float(scale), _sptr(stream))
+
+    def decode_append_attention(self, layer, reqs, k_new, v_new, q, out, scale, stream=None) -> int:
+        """kv_append of one token per request + attention, fused in one launch."""
+        r = _i32(reqs)
+        return ellm_decode_append_attention(self._h, layer, len(r), _ptr(r), _dptr(k_new), _dptr(v_new),
+                                            _dptr(q), _dptr(out), float(scale), _sptr(stream))
 
     def release(self, req, stream=None) -> int:
         return ellm_release(self._h, int(req), _sptr(stream))

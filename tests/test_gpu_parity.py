@@ -168,7 +168,7 @@ def test_vmm_grow_shrink_and_alias_view():
     """pool_grow / pool_shrink map and unmap 2 MiB chunks (cuMemMap/cuMemUnmap); the alias
     view maps a request's chunks contiguously (the paper's KV eTensor)."""
     import torch
-    t = Twin(32, 32, 8, 128, 16, 16, 6, 2, 8, 2, seed=4)
+    t = Twin(32, 32, 8, 128, 16, 16, 6, 2, 8, 2, seed=4, map_unit_bytes=2 << 20)
     assert t.p.chunk_bytes == 2 << 20
     s0 = t.p.stats()
     assert s0["mapped_bytes"] == 6 * (2 << 20) and s0["n_map"] == 6
@@ -214,3 +214,30 @@ def test_error_codes_match_oracle_on_device():
     assert t.inflate([1])[0] == -6
     t.check_tables()
     t.check_bytes()
+
+
+FUSED_SHAPES = [(2, 32, 8, 128, 16), (1, 64, 8, 128, 32), (1, 8, 2, 128, 16), (1, 8, 1, 128, 256),
+                (2, 4, 2, 64, 16), (1, 16, 16, 128, 16)]
+
+
+@pytest.mark.parametrize("shape", FUSED_SHAPES, ids=[str(s) for s in FUSED_SHAPES])
+def test_fused_decode_append_attention(shape):
+    """ellm_decode_append_attention == kv_append + attention: bytes bit-exact (the new row lands
+    in its chunk), attention within tolerance, for decode steps crossing chunk boundaries."""
+    L, Hq, Hkv, d, T = shape
+    lens = [1, 15, 16, 31, 300, 2047]
+    R = len(lens)
+    mc = max((x + 40 + T - 1) // T for x in lens)
+    t = Twin(L, Hq, Hkv, d, T, R * mc + 4, R * mc + 4, R, mc, 0, seed=21)
+    reqs = list(range(R))
+    assert t.reserve(reqs, lens) == 0
+    t.append_all_layers(reqs, lens)
+    for step in range(20):
+        assert t.reserve(reqs, [1] * R) == 0
+        for l in range(L):
+            assert t.decode_fused(l, reqs[::-1] if step % 2 else reqs) == 0
+    t.check_tables()
+    t.check_bytes()
+    # precondition: the latest reservation must be exactly one token
+    assert t.reserve([0], [2]) == 0
+    assert t.decode_fused(0, [0]) == -1

@@ -40,11 +40,11 @@ def check_attention(out_bits: np.ndarray, ref: np.ndarray, what=""):
 
 class Twin:
     def __init__(self, L, Hq, Hkv, d, T, C, Ckv, R, MC, H, seed=0, needle=True, device=0,
-                 q_head0=0, kv_head0=0, group=None):
+                 q_head0=0, kv_head0=0, group=None, map_unit_bytes=0):
         from paper_2506_15155_b200 import ellm
         self.ellm = ellm
         self.o = Oracle(L, Hq, Hkv, d, T, C, Ckv, R, MC, H)
-        self.p = ellm.Pool(device, L, Hq, Hkv, d, T, C, Ckv, R, MC, H)
+        self.p = ellm.Pool(device, L, Hq, Hkv, d, T, C, Ckv, R, MC, H, map_unit_bytes)
         self.L, self.Hq, self.Hkv, self.d, self.T, self.R = L, Hq, Hkv, d, T, R
         self.group = group or Hq // Hkv
         self.seed, self.needle = seed, needle
@@ -100,6 +100,22 @@ class Twin:
         if check:
             check_attention(got, ref, f"layer {layer} reqs {list(reqs)[:8]}")
         return 0, (got, ref)
+
+    def decode_fused(self, layer, reqs):
+        """Oracle: append of the pending token + attention; product: the fused single launch."""
+        import torch
+        K, V = self.kv_rows(reqs, [1] * len(reqs), layer)
+        q = self.q_bits(reqs, layer)
+        a = self.o.append(layer, reqs, [1] * len(reqs), K, V)
+        rc_o, ref = self.o.attention(layer, reqs, q, self.scale) if a == 0 else (a, None)
+        out = torch.full((len(reqs), self.Hq, self.d), float("nan"), dtype=torch.bfloat16, device="cuda")
+        rc_p = self.p.decode_append_attention(layer, reqs, bits_to_torch(K), bits_to_torch(V),
+                                              bits_to_torch(q), out, self.scale)
+        torch.cuda.synchronize()
+        assert rc_o == rc_p, (rc_o, rc_p)
+        if rc_o == 0:
+            check_attention(torch_to_bits(out), ref, f"fused layer {layer} reqs {list(reqs)[:8]}")
+        return rc_o
 
     def deflate(self, ids):
         (a, sa), (b, sb) = self.o.deflate(ids), self.p.deflate(ids)
