@@ -34,8 +34,11 @@ constexpr int kThreads = (kConsumerWarps + 1) * 32;
 
 __host__ __device__ constexpr int stages_for(int D) { return D == 128 ? 3 : 6; }
 __host__ __device__ constexpr int stage_bytes_for(int D) { return 2 * 128 * D * 2; }  // HB*TT = 128
+constexpr int kQSlots = 2;  // Q ring: one slot per in-flight (owner, request) segment
+__host__ __device__ constexpr int q_slot_bytes_for(int D) { return 8 * 8 * D * 2; }  // HB*group <= 64 rows
 __host__ __device__ constexpr int smem_bytes_for(int D) {
-  return stages_for(D) * stage_bytes_for(D) + 1024 /*align*/ + 2 * 8 * stages_for(D);
+  return stages_for(D) * stage_bytes_for(D) + kQSlots * q_slot_bytes_for(D) + 1024 /*align*/ +
+         8 * (2 * stages_for(D) + 2 * kQSlots);
 }
 
 // token permutation inside a 16-token subtile: column c of the S tile holds
@@ -86,6 +89,12 @@ __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar),
       "l"(policy)
       : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
 }
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 v;
@@ -149,7 +158,8 @@ constexpr int kFirst = 1, kLast = 2, kDone = 4;  // stage metadata flags
 // row is one coalesced D*4-byte load across the row's lanes. Records written by other SMs are
 // read through L2 (__ldcg): L1 is not coherent across SMs.
 template <int D>
-__device__ __forceinline__ void merge_request(const Params& p, int vr, int rows, int nsub, int HB) {
+__device__ __forceinline__ void merge_request(const Params& p, int vr, int rows, int nsub, int HB, int w0,
+                                              int nw) {  // run by warps [w0, w0 + nw)
   constexpr int LPR = D / 4;         // lanes per row
   constexpr int RPW = 32 / LPR;      // rows per warp pass
   // record ranges: static owners (CTAs b), then dynamic owners (units u); record id of
@@ -164,7 +174,7 @@ __device__ __forceinline__ void merge_request(const Params& p, int vr, int rows,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int e4 = lane % LPR, sub = lane / LPR;
   const unsigned seg_mask = RPW == 1 ? 0xffffffffu : (0xffffu << (16 * sub));
-  for (int row0 = warp * RPW; row0 < rows; row0 += kConsumerWarps * RPW) {
+  for (int row0 = (warp - w0) * RPW; row0 < rows; row0 += nw * RPW) {
     const int row = row0 + sub;
     const bool live = row < rows;
     float M = -INFINITY;
@@ -230,13 +240,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int NB = D / 64;            // V blocks per lane
   constexpr int NT = D / 8;             // PV n-tiles
 
+  constexpr int QB = q_slot_bytes_for(D);
+  constexpr int kMaxMerges = 64;        // deferred merges per CTA (the list is flushed when full)
+
   extern __shared__ uint8_t smem_raw[];
-  __shared__ int s_last;
-  __shared__ int4 s_meta[NST];          // per stage: {vr, tile within vr, record owner, flags}
+  __shared__ int4 s_meta[NST];          // per stage: {vr, tile within vr, record owner, flags | qslot}
+  __shared__ int s_merge[kMaxMerges];   // requests this CTA completed last (merged at the end)
+  __shared__ int s_n_merge;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * SB);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * SB + kQSlots * QB);
   const uint32_t sbase = smem_u32(smem);
+  const uint32_t qbase = sbase + NST * SB;  // Q ring: kQSlots x QB bytes
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + NST);
+  const uint32_t qfull0 = smem_u32(bars + 2 * NST), qempty0 = smem_u32(bars + 2 * NST + kQSlots);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -244,6 +260,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, kConsumerWarps);
     }
+    for (int s = 0; s < kQSlots; ++s) {
+      mbar_init(qfull0 + 8 * s, 1);
+      mbar_init(qempty0 + 8 * s, kConsumerWarps);
+    }
+    s_n_merge = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -272,9 +293,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int32_t* cum = p.cum_s;
     unsigned long long next_ticket = 0;
     if (p.n_dyn > 0 && lane == 0) next_ticket = atomicAdd(p.ticket, 1ull);
+    uint32_t segc = 0;  // segments started (selects the Q slot and its parity)
     for (;;) {
       int vr = find_vr(cum, p.n_vr, t_begin);
-      for (int64_t tile = t_begin; tile < t_end; ++vr) {
+      for (int64_t tile = t_begin; tile < t_end; ++vr, ++segc) {
         const int64_t seg_end = min(t_end, int64_t(__ldg(cum + vr + 1)));
         const int ireq = vr / p.HG, hg = vr % p.HG;
         const int32_t len = __ldg(p.len + ireq);
@@ -282,10 +304,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         // space coordinate of the request's first tile in this space, minus its tile offset
         const int64_t tile0 = __ldg(cum + vr) -
                               (cum == p.cum_d ? int64_t(__ldg(p.cum_s + vr + 1) - __ldg(p.cum_s + vr)) : 0);
-        {  // warm L1 with this segment's Q rows for the consumers (they read them at FIRST)
-          const char* qb = reinterpret_cast<const char*>(p.q + (int64_t(ireq) * p.Hq + hg * HB * p.group) * D);
-          for (int off = lane * 128; off < HB * p.group * D * 2; off += 32 * 128)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(qb + off));
+        const int qs = int(segc % kQSlots);
+        if (lane == 0) {  // stage this segment's Q rows (HB*group x D, contiguous) into its slot
+          mbar_wait(qempty0 + 8 * qs, ((segc / kQSlots) & 1) ^ 1);
+          const uint32_t qbytes = uint32_t(HB * p.group * D * 2);
+          mbar_expect_tx(qfull0 + 8 * qs, qbytes);
+          bulk_load(qbase + qs * QB, p.q + (int64_t(ireq) * p.Hq + hg * HB * p.group) * D, qbytes,
+                    qfull0 + 8 * qs);
         }
         for (int64_t t = tile; t < seg_end; t += 32) {
           const int cnt = int(min(int64_t(32), seg_end - t));
@@ -330,7 +355,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               mbar_wait(empty0 + 8 * stage, phase ^ 1);
               const int64_t tl = t + u;
               s_meta[stage] = make_int4(vr, int(tl - tile0), owner + vr,
-                                        (tl == tile ? kFirst : 0) | (tl == seg_end - 1 ? kLast : 0));
+                                        (tl == tile ? kFirst : 0) | (tl == seg_end - 1 ? kLast : 0) |
+                                            int((segc & 0xffff) << 8));
               int npc = 0;
 #pragma unroll
               for (int k = 0; k < 8; ++k) npc += (k < npieces && e[k] >= 0);
@@ -402,17 +428,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (meta.w & kDone) break;
     const int vr = meta.x;
     if (meta.w & kFirst) {  // a new (owner, request) segment: its Q and fresh softmax state
-      const int ireq = vr / p.HG, hg = vr % p.HG;
+      const int ireq = vr / p.HG;
       len = __ldg(p.len + ireq);
+      const uint32_t segc = uint32_t(meta.w) >> 8;  // Q rows were staged by the producer
+      const int qs = int(segc % kQSlots);
+      mbar_wait(qfull0 + 8 * qs, (segc / kQSlots) & 1);
       if (g < p.group) {
-        const uint4* qrow = reinterpret_cast<const uint4*>(
-            p.q + (int64_t(ireq) * p.Hq + hg * HB * p.group + row) * D);
+        const uint32_t qrow = qbase + qs * QB + uint32_t(row * D * 2);
 #pragma unroll
-        for (int i = 0; i < KI; ++i) qb[i] = __ldg(qrow + kblock<D>(q, i));
+        for (int i = 0; i < KI; ++i) qb[i] = lds128(qrow + 16 * kblock<D>(q, i));
       } else {
 #pragma unroll
         for (int i = 0; i < KI; ++i) qb[i] = make_uint4(0, 0, 0, 0);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(qempty0 + 8 * qs);
 #pragma unroll
       for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
       m_run = -INFINITY;
@@ -522,21 +552,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (q == 0) *reinterpret_cast<float2*>(p.part_ml + rec * 2) = make_float2(m_run, l_tot);
     }
-    // ---- arrival: the last owner to finish request vr merges its records (a5, fused) ----
-    __threadfence();  // publish this lane's records at GPU scope before the arrival
+    // ---- arrival: the owner that completes request vr's count merges it (a5, fused) ----
+    // bar.sync orders every consumer's record stores before thread 0's gpu-scope fence +
+    // atomic (fences are cumulative); only warp 0 waits for the atomic's result, and the merge
+    // itself is deferred to the end of this CTA's work so segment switches stay cheap.
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
-    if (threadIdx.x == 0) {
-      const int bf = __ldg(p.b_first + vr), bl = __ldg(p.b_last + vr);
-      const int uf = __ldg(p.u_first + vr), ul = __ldg(p.u_last + vr);
-      const int owners = (bl >= bf ? bl - bf + 1 : 0) + (ul >= uf ? ul - uf + 1 : 0);
-      const int old = atomicAdd(p.arrivals + vr, 1);
-      s_last = (old == owners - 1);
-      if (s_last) p.arrivals[vr] = 0;  // every owner of vr has arrived: re-arm for the next launch
-      __threadfence();
+    if (warp == 0) {
+      int now = 0;
+      if (lane == 0) {
+        __threadfence();
+        const int bf = __ldg(p.b_first + vr), bl = __ldg(p.b_last + vr);
+        const int uf = __ldg(p.u_first + vr), ul = __ldg(p.u_last + vr);
+        const int owners = (bl >= bf ? bl - bf + 1 : 0) + (ul >= uf ? ul - uf + 1 : 0);
+        const int old = atomicAdd(p.arrivals + vr, 1);
+        if (old == owners - 1) {
+          p.arrivals[vr] = 0;  // every owner of vr has arrived: re-arm for the next launch
+          __threadfence();
+          if (s_n_merge < kMaxMerges) s_merge[s_n_merge++] = vr;
+          else now = 1;        // deferred list full: warp 0 merges this one right away
+        }
+      }
+      if (__shfl_sync(0xffffffffu, now, 0)) merge_request<D>(p, vr, rows, NSUB, HB, 0, 1);
     }
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
-    if (s_last) merge_request<D>(p, vr, rows, NSUB, HB);
   }
+  // ---- end of this CTA's work: all consumer warps merge the requests it completed ----
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+  __threadfence();
+  for (int k = 0; k < s_n_merge; ++k) merge_request<D>(p, s_merge[k], rows, NSUB, HB, 0, kConsumerWarps);
 }
 
 template <int D, int HB>

@@ -216,11 +216,14 @@ int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out) {
   const int64_t g64 = int64_t(gran);
   int64_t lcm = p->chunk_bytes;
   while (lcm % g64 != 0) lcm += p->chunk_bytes;
-  if (c.map_unit_bytes > 0) {
-    if (c.map_unit_bytes % lcm != 0) return fail(ELLM_ERR_UNSUPPORTED);
-    p->unit_bytes = c.map_unit_bytes;
+  int64_t want_unit = c.map_unit_bytes;
+  if (want_unit == 0)
+    if (const char* v = std::getenv("ELLM_MAP_UNIT_BYTES")) want_unit = std::atol(v);  // experiments
+  if (want_unit > 0) {
+    if (want_unit % lcm != 0) return fail(ELLM_ERR_UNSUPPORTED);
+    p->unit_bytes = want_unit;
   } else {
-    p->unit_bytes = lcm * ((int64_t(64) << 20) + lcm - 1) / lcm;
+    p->unit_bytes = lcm * (((int64_t(64) << 20) + lcm - 1) / lcm);
     const int64_t pool_bytes = ((c.max_chunks * p->chunk_bytes + lcm - 1) / lcm) * lcm;
     p->unit_bytes = std::min(p->unit_bytes, pool_bytes);
   }

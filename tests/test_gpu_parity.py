@@ -241,3 +241,24 @@ def test_fused_decode_append_attention(shape):
     # precondition: the latest reservation must be exactly one token
     assert t.reserve([0], [2]) == 0
     assert t.decode_fused(0, [0]) == -1
+
+
+def test_map_units_follow_ownership():
+    """Default map units (64 MiB = 32 chunks of 2 MiB): a unit is mapped when its first chunk
+    becomes KV and unmapped when its last chunk returns to ACT; bytes survive."""
+    MB2 = 2 << 20
+    t = Twin(32, 32, 8, 128, 16, 100, 40, 3, 16, 0, seed=8)
+    s = t.p.stats()
+    assert s["mapped_bytes"] == 2 * 32 * MB2 and s["n_map"] == 2      # chunks 0..63 -> units 0, 1
+    assert t.grow(30) == 0                                             # chunks 40..69 -> unit 2
+    assert t.p.stats()["n_map"] == 3
+    assert t.reserve([0, 1], [16 * 16, 16 * 10]) == 0
+    t.append_all_layers([0, 1], [16 * 16, 16 * 10])
+    assert t.shrink(44) == 0                                           # FREE 26..69 -> ACT
+    s = t.p.stats()
+    assert s["n_unmap"] == 2 and s["mapped_bytes"] == 32 * MB2        # units 1, 2 released
+    assert t.grow(40) == 0                                             # 26..65: units 1, 2 back
+    assert t.p.stats()["n_map"] == 5
+    t.check_tables()
+    t.check_bytes()
+    t.attention(31, [0, 1])
