@@ -23,10 +23,13 @@
  *     HOST pointers, read/written before the call returns. Tensors (q, k_new, v_new, out)
  *     are DEVICE pointers owned by the caller; they must stay valid until the stream
  *     reaches the enqueued work. `stream` is a cudaStream_t (NULL = legacy default stream).
- *   - Device work is enqueued on `stream` and ordered only by it. A chunk or host slot
- *     freed by one call may be handed out by the next call; if those calls use different
- *     streams the caller orders them (events). Kernel faults surface as ELLM_ERR_CUDA at a
- *     later call (ellm_last_cuda_error gives the cudaError_t).
+ *   - Device work is enqueued on `stream`. Reuse is stream-ordered by the library: a chunk or
+ *     host slot freed by work on stream A (deflate, inflate, migrate, release) carries the event
+ *     recorded after that work, and a later call on stream B that is handed it makes B wait on
+ *     that event first (allocation order itself stays deterministic). Work on the same request
+ *     from two streams must still be ordered by the caller. Attention calls on one pool share
+ *     its split-K workspace and must be ordered among themselves. Kernel faults surface as
+ *     ELLM_ERR_CUDA at a later call (ellm_last_cuda_error gives the cudaError_t).
  *   - One pool per device; calls on one pool are externally serialised.
  *   - Allocation policy (R7): lowest free chunk id / host slot first, requests in
  *     the given order, positions ascending. Tables are therefore deterministic and identical

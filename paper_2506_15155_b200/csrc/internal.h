@@ -192,8 +192,20 @@ struct ellm_pool {
   ellm::AttnPlan cache_plan;
   unsigned long long* d_ticket = nullptr;  // dynamic-unit ticket counter (device)
   uint64_t ticket_base = 0;                // tickets consumed by earlier launches
-  int64_t dyn_div = 8;                     // dynamic tail = W / dyn_div tiles (0: static only)
+  int64_t dyn_div = 0;                     // dynamic tail = tiles/dyn_div per request (0: static only)
   int64_t dyn_unit = 8;                    // minimum tiles per dynamic unit
+
+  // stream-ordered reuse: a chunk / host slot freed by work on stream S carries the event
+  // recorded after that work; a later call on another stream that allocates it first makes
+  // its stream wait on the event (allocation order itself stays deterministic).
+  struct FreeEvent {
+    cudaEvent_t ev = nullptr;
+    cudaStream_t stream = nullptr;
+    int32_t refs = 0;
+  };
+  std::vector<FreeEvent> free_events;
+  std::vector<int32_t> free_event_pool;          // indices of unreferenced events
+  std::vector<int32_t> chunk_ev, slot_ev;        // per chunk / host slot: event index or -1
 
   std::map<int32_t, std::pair<CUdeviceptr, size_t>> alias;
   int last_cuda_error = 0;

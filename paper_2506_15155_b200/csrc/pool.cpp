@@ -86,6 +86,45 @@ void free_host(ellm_pool* p, int64_t h) {
 
 cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// ---- stream-ordered reuse of freed chunks / host slots (see ellm_pool::FreeEvent) ----------
+// Record an event on `stream` after the work that frees some chunks / slots; returns its index.
+int32_t record_free_event(ellm_pool* p, cudaStream_t stream) {
+  int32_t i;
+  if (!p->free_event_pool.empty()) {
+    i = p->free_event_pool.back();
+    p->free_event_pool.pop_back();
+  } else {
+    ellm_pool::FreeEvent fe;
+    if (cudaEventCreateWithFlags(&fe.ev, cudaEventDisableTiming) != cudaSuccess) return -1;
+    p->free_events.push_back(fe);
+    i = int32_t(p->free_events.size()) - 1;
+  }
+  ellm_pool::FreeEvent& fe = p->free_events[size_t(i)];
+  fe.stream = stream;
+  fe.refs = 0;
+  if (cudaEventRecord(fe.ev, stream) != cudaSuccess) return -1;
+  return i;
+}
+void drop_ref(ellm_pool* p, int32_t i) {
+  if (i >= 0 && --p->free_events[size_t(i)].refs == 0) p->free_event_pool.push_back(i);
+}
+void attach_event(ellm_pool* p, std::vector<int32_t>& tag, int64_t id, int32_t i) {
+  drop_ref(p, tag[size_t(id)]);
+  tag[size_t(id)] = i;
+  if (i >= 0) ++p->free_events[size_t(i)].refs;
+}
+// Before work on `stream` touches a newly allocated chunk / slot: wait for its freeing work
+// if that ran on another stream.
+cudaError_t wait_freed(ellm_pool* p, std::vector<int32_t>& tag, int64_t id, cudaStream_t stream) {
+  const int32_t i = tag[size_t(id)];
+  if (i < 0) return cudaSuccess;
+  cudaError_t e = cudaSuccess;
+  if (p->free_events[size_t(i)].stream != stream) e = cudaStreamWaitEvent(stream, p->free_events[size_t(i)].ev, 0);
+  tag[size_t(id)] = -1;
+  drop_ref(p, i);
+  return e;
+}
+
 // Upload pending table updates (snapshots of host entries) and scatter them on `stream`.
 int flush_table(ellm_pool* p, cudaStream_t stream) {
   if (!p->has_dev) {
@@ -190,6 +229,8 @@ int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out) {
   p->hused.assign(size_t(c.host_slots), 0);
   p->slot_req.assign(size_t(c.host_slots), -1);
   p->slot_idx.assign(size_t(c.host_slots), -1);
+  p->chunk_ev.assign(size_t(c.max_chunks), -1);
+  p->slot_ev.assign(size_t(c.host_slots), -1);
   p->table.assign(size_t(int64_t(c.max_requests) * c.max_chunks_per_request), UNMAPPED);
   p->len.assign(size_t(c.max_requests), 0);
   p->pending.assign(size_t(c.max_requests), 0);
@@ -294,6 +335,8 @@ int ellm_pool_destroy(ellm_pool* p) {
       ellm_unalias_request(p, r);
     }
     p->ring.destroy();
+    for (auto& fe : p->free_events)
+      if (fe.ev) cudaEventDestroy(fe.ev);
     if (p->d_table) cudaFree(p->d_table);
     if (p->d_part) cudaFree(p->d_part);
     if (p->d_part_ml) cudaFree(p->d_part_ml);
@@ -364,6 +407,7 @@ int ellm_kv_reserve(ellm_pool* p, int32_t n, const int32_t* reqs, const int32_t*
       p->chunk_req[size_t(c)] = r;
       p->chunk_idx[size_t(c)] = int32_t(ci);
       set_entry(p, r, ci, int32_t(c));
+      if (p->has_dev && wait_freed(p, p->chunk_ev, c, S(stream)) != cudaSuccess) return ELLM_ERR_CUDA;
     }
     p->len[size_t(r)] = L + n_new[i];
     p->pending[size_t(r)] = n_new[i];
@@ -553,14 +597,22 @@ extern "C" {
 
 // O8 — released slots return to the pool.
 int ellm_release(ellm_pool* p, int32_t r, void* stream) {
-  (void)stream;
   if (!p) return ELLM_ERR_INVALID_ARG;
   if (r < 0 || r >= p->cfg.max_requests) return ELLM_ERR_OUT_OF_RANGE;
   int64_t nc = nchunks_of(p, p->len[size_t(r)]);
+  // the request's chunks / slots are free once `stream` reaches this point
+  const int32_t ev = (p->has_dev && nc > 0) ? record_free_event(p, S(stream)) : -1;
+  if (p->has_dev && nc > 0 && ev < 0) return ELLM_ERR_CUDA;
   for (int64_t i = 0; i < nc; ++i) {
     int32_t e = entry_c(p, r, i);
-    if (is_dev(e)) free_chunk(p, e);
-    if (is_host(e)) free_host(p, host_of(e));
+    if (is_dev(e)) {
+      free_chunk(p, e);
+      attach_event(p, p->chunk_ev, e, ev);
+    }
+    if (is_host(e)) {
+      free_host(p, host_of(e));
+      attach_event(p, p->slot_ev, host_of(e), ev);
+    }
     entry(p, r, i) = UNMAPPED;  // device mirror rows beyond len are never read
   }
   p->len[size_t(r)] = 0;
@@ -595,6 +647,8 @@ int ellm_deflate(ellm_pool* p, int32_t n, const int32_t* ids, int32_t* slots_out
   }
   if (!p->has_dev || n == 0) return flush_table(p, S(stream));
   cudaError_t e;
+  for (int32_t h : dst)  // a slot last read by an inflate on another stream
+    if ((e = wait_freed(p, p->slot_ev, h, S(stream))) != cudaSuccess) return cuda_fail(p, e);
   uint8_t* pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
   if (p->swap_mode == 1) {
     for (int32_t i = 0; i < n; ++i)
@@ -616,6 +670,11 @@ int ellm_deflate(ellm_pool* p, int32_t n, const int32_t* ids, int32_t* slots_out
         cudaSuccess)
       return cuda_fail(p, e);
     ++p->launches;
+  }
+  {  // the source chunks are free once the copy-out on `stream` is done
+    const int32_t ev = record_free_event(p, S(stream));
+    if (ev < 0) return ELLM_ERR_CUDA;
+    for (int32_t c : src) attach_event(p, p->chunk_ev, c, ev);
   }
   return flush_table(p, S(stream));
 }
@@ -645,6 +704,8 @@ int ellm_inflate(ellm_pool* p, int32_t n, const int32_t* slots, int32_t* ids_out
   }
   if (!p->has_dev || n == 0) return flush_table(p, S(stream));
   cudaError_t e;
+  for (int32_t c : dst)  // a chunk freed by work on another stream
+    if ((e = wait_freed(p, p->chunk_ev, c, S(stream))) != cudaSuccess) return cuda_fail(p, e);
   uint8_t* pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
   if (p->swap_mode == 1) {
     for (int32_t i = 0; i < n; ++i)
@@ -666,6 +727,11 @@ int ellm_inflate(ellm_pool* p, int32_t n, const int32_t* slots, int32_t* ids_out
         cudaSuccess)
       return cuda_fail(p, e);
     ++p->launches;
+  }
+  {  // the source host slots are free once the copy-in on `stream` is done
+    const int32_t ev = record_free_event(p, S(stream));
+    if (ev < 0) return ELLM_ERR_CUDA;
+    for (int32_t h : src) attach_event(p, p->slot_ev, h, ev);
   }
   return flush_table(p, S(stream));
 }
@@ -698,13 +764,21 @@ int ellm_migrate(ellm_pool* p, int32_t n, const int32_t* src, const int32_t* dst
     free_chunk(p, s);
   }
   if (!p->has_dev || n == 0) return flush_table(p, S(stream));
+  cudaError_t e;
+  for (int32_t i = 0; i < n; ++i)  // destinations freed by work on another stream
+    if ((e = wait_freed(p, p->chunk_ev, dst[i], S(stream))) != cudaSuccess) return cuda_fail(p, e);
   const int32_t* dd;
   int rc = upload_ints(p, all, S(stream), &dd, nullptr);
   if (rc) return rc;
   uint8_t* pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
-  cudaError_t e = launch_chunk_copy(pool, dd + n, pool, dd, n, p->chunk_bytes, 2 * p->num_sms, S(stream));
+  e = launch_chunk_copy(pool, dd + n, pool, dd, n, p->chunk_bytes, 2 * p->num_sms, S(stream));
   if (e != cudaSuccess) return cuda_fail(p, e);
   ++p->launches;
+  {  // the source chunks are free once the copy on `stream` is done
+    const int32_t ev = record_free_event(p, S(stream));
+    if (ev < 0) return ELLM_ERR_CUDA;
+    for (int32_t i = 0; i < n; ++i) attach_event(p, p->chunk_ev, src[i], ev);
+  }
   return flush_table(p, S(stream));
 }
 

@@ -243,6 +243,25 @@ def test_fused_decode_append_attention(shape):
     assert t.decode_fused(0, [0]) == -1
 
 
+@pytest.mark.parametrize("div", [8, 3])
+def test_dynamic_tail_schedule(div, monkeypatch):
+    """The optional dynamic-tail schedule (ELLM_ATTN_DYN_DIV): the last
+    tiles/div tiles of every request are claimed in units by whichever CTA is free; results
+    must match the oracle exactly as the static schedule does (also fused decode)."""
+    monkeypatch.setenv("ELLM_ATTN_DYN_DIV", str(div))
+    lens = [4000, 3001, 17, 2500, 1]
+    R = len(lens)
+    t = Twin(1, 32, 8, 128, 16, 800, 800, R, 260, 0, seed=13)
+    reqs = list(range(R))
+    assert t.reserve(reqs, lens) == 0
+    t.append_all_layers(reqs, lens)
+    for _ in range(3):
+        t.attention(0, reqs)           # ticket counter advances across launches
+    assert t.reserve(reqs, [1] * R) == 0
+    assert t.decode_fused(0, reqs[::-1]) == 0
+    t.check_bytes()
+
+
 def test_map_units_follow_ownership():
     """Default map units (64 MiB = 32 chunks of 2 MiB): a unit is mapped when its first chunk
     becomes KV and unmapped when its last chunk returns to ACT; bytes survive."""

@@ -1,0 +1,70 @@
+"""Stream-ordered reuse (include/ellm.h "Conventions"): chunks freed by a deflate on one stream
+and immediately handed to a reserve + append on another stream must not be overwritten
+before the copy-out has read them; host slots freed by an inflate likewise."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _fill(pool, wl, r, n, stream):
+    import torch
+    from inputs import workload as W
+    row = wl.hkv_local * wl.head_dim * 2
+    kb = torch.empty((n, wl.hkv_local, wl.head_dim), dtype=torch.bfloat16, device="cuda")
+    vb = torch.empty_like(kb)
+    s = stream.cuda_stream
+    for l in range(wl.n_layers):
+        W.gen_kv_device(wl, r, 0, n, l, 0, kb.data_ptr(), s)
+        W.gen_kv_device(wl, r, 0, n, l, 1, vb.data_ptr(), s)
+        assert pool.append(l, [r], [n], kb, vb, s) == 0
+    del row
+    return kb, vb
+
+
+def _check_chunk(img, wl, r, i, T=16):
+    from inputs import gen
+    img = img.view(np.uint16).reshape(wl.n_layers, 2, wl.hkv_local, T, wl.head_dim)
+    pos = np.arange(i * T, (i + 1) * T)
+    for l in (0, wl.n_layers - 1):
+        for kv in (0, 1):
+            want = gen.kv_bits(wl.seed, r, pos, l, kv, range(wl.hkv_local), wl.head_dim, wl.group, 0)
+            assert np.array_equal(img[l, kv].transpose(1, 0, 2), want), (r, i, l, kv)
+
+
+def test_deflate_then_reuse_on_another_stream():
+    import torch
+    from inputs import workload as W
+    from paper_2506_15155_b200 import ellm
+    wl = W.Workload("streams", 32, 32, 8, 128, 2, 32000, seed=9, needle=False)
+    n_chunks = 2000
+    pool = ellm.Pool(0, 32, 32, 8, 128, 16, 2 * n_chunks + 8, 2 * n_chunks + 8, 2, n_chunks, n_chunks)
+    s0, s1, s2 = torch.cuda.current_stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    assert pool.reserve([0], [wl.context], s0.cuda_stream) == 0
+    _fill(pool, wl, 0, wl.context, s0)
+    torch.cuda.synchronize()
+    ids_a = pool.table(0)[0].tolist()
+    # ~4 GiB copy-out on s1, and request 1 immediately takes the freed chunks on s2
+    rc, slots = pool.deflate(ids_a, s1.cuda_stream)
+    assert rc == 0
+    assert pool.reserve([1], [wl.context], s2.cuda_stream) == 0
+    assert sorted(pool.table(1)[0].tolist()) == sorted(ids_a)[: len(ids_a)]  # lowest ids reused
+    kb, vb = _fill(pool, wl, 1, wl.context, s2)
+    torch.cuda.synchronize()
+    for i in (0, 999, n_chunks - 1):
+        _check_chunk(pool.read_host_slot(int(slots[i])), wl, 0, i)             # A intact on host
+        _check_chunk(pool.read_chunk(int(pool.table(1)[0][i])), wl, 1, i)      # B in the chunks
+    # inflate A back on s1 into free chunks, then B's release + a new deflate on s2 reuses
+    # A's freed host slots: the new copy-out must wait for the copy-in that reads them
+    pool.release(1, s2.cuda_stream)
+    rc, ids_back = pool.inflate(slots, s1.cuda_stream)
+    assert rc == 0
+    assert pool.reserve([1], [wl.context], s2.cuda_stream) == 0
+    _fill(pool, wl, 1, wl.context, s2)
+    rc, slots_b = pool.deflate(pool.table(1)[0].tolist(), s2.cuda_stream)
+    assert rc == 0 and sorted(slots_b.tolist()) == sorted(slots.tolist())
+    torch.cuda.synchronize()
+    for i in (0, 1234, n_chunks - 1):
+        _check_chunk(pool.read_chunk(int(ids_back[i])), wl, 0, i)
+        _check_chunk(pool.read_host_slot(int(slots_b[i])), wl, 1, i)
+    pool.close()
