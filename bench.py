@@ -224,11 +224,16 @@ def main():
     B, L = wl.batch, wl.n_layers
     swap_chunks = 1024 if not args.no_swap else 0
     t_create = time.perf_counter()
-    pool = W.make_pool(wl, local, host_slots=swap_chunks)
+    # + one extra request (id = batch) of swap_chunks chunks: the swap / migrate measurements
+    # move it between HBM and pinned host memory while the decode set stays resident
+    pool = W.make_pool(wl, local, host_slots=swap_chunks, extra_chunks=swap_chunks,
+                       extra_requests=1 if swap_chunks else 0)
     t_create = time.perf_counter() - t_create
     st_create = pool.stats()
     prefill_appends = []
     W.prefill(pool, wl, append_times=prefill_appends)
+    if swap_chunks:
+        W.fill_request(pool, wl, wl.batch, swap_chunks * wl.tokens_per_chunk)
     reqs = list(range(B))
     ones = [1] * B
     scale = 1.0 / (wl.head_dim ** 0.5)
@@ -236,6 +241,8 @@ def main():
     n_steps = args.warmup + args.steps
     e2e_steps = 0 if args.no_e2e else args.steps
     UNFUSED_STEPS = 3  # comparison: separate kv_append + attention launches
+    CONC_STEPS = 10 if swap_chunks else 0  # decode steps with a concurrent swap stream
+    e2e_steps += CONC_STEPS
     e2e_steps += UNFUSED_STEPS
     inputs = []
     for s in range(n_steps + e2e_steps):
@@ -339,7 +346,7 @@ def main():
 
     # ---- end to end through host buffers: H2D of each step's inputs, D2H of its outputs ----
     e2e = None
-    n_e2e = e2e_steps - UNFUSED_STEPS
+    n_e2e = e2e_steps - UNFUSED_STEPS - CONC_STEPS
     if n_e2e:
         hin = []
         for s in range(n_steps, n_steps + n_e2e):
@@ -368,6 +375,41 @@ def main():
                "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ems / n_e2e, 3)}
 
     swap = measure_swap(pool, wl, stream) if swap_chunks else None
+
+    # ---- swap overlapped with decode: the extra request is deflated / inflated on a second
+    #      stream (3 rounds of 2 x 2 GiB) while CONC_STEPS decode steps run on the compute stream
+    if swap_chunks:
+        conc = {}
+        c_first = n_steps + n_e2e
+        for mode, name in ((1, "ce"), (0, "sm")):
+            pool.set_swap_mode(mode)
+            ss = torch.cuda.Stream()
+            barrier()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(ss)
+            d0.record(stream)
+            moved = 0
+            for _ in range(3):
+                rc, slots = pool.deflate(pool.table(wl.batch)[0].tolist(), ss.cuda_stream)
+                assert rc == ellm.OK, rc
+                rc, _ = pool.inflate(slots, ss.cuda_stream)
+                assert rc == ellm.OK, rc
+                moved += 2 * len(slots) * pool.chunk_bytes
+            s1.record(ss)
+            half = CONC_STEPS // 2  # 5 steps per mode, consecutive positions
+            base = c_first + (0 if mode == 1 else half)
+            for s in range(base, base + half):
+                step(*inputs[s])
+            d1.record(stream)
+            barrier()
+            swap_ms, dec_ms = s0.elapsed_time(s1), d0.elapsed_time(d1)
+            conc[name] = {"decode_ms_per_step": round(dec_ms / half, 3), "swap_gbs": round(moved / swap_ms / 1e6, 2),
+                          "swap_ms": round(swap_ms, 2), "decode_ms": round(dec_ms, 2)}
+        pool.set_swap_mode(0)
+        swap["concurrent_with_decode"] = {
+            "isolated_decode_ms_per_step": round(ms_step, 4), **conc,
+            "note": "3 rounds of deflate+inflate of 1024 x 2 MiB on a second stream during decode"}
 
     # ---- unfused comparison: the same step as separate kv_append and attention launches ----
     barrier()
@@ -452,7 +494,7 @@ def measure_swap(pool, wl, stream):
         pool.set_swap_mode(mode)
         best_d2h, best_h2d, best_mig = 0.0, 0.0, 0.0
         for _ in range(3):
-            ids = pool.table(0)[0][:n].tolist()
+            ids = pool.table(wl.batch)[0][:n].tolist()  # the extra (non-decoding) request
             t, (rc, slots) = timed(lambda: pool.deflate(ids, sp))
             assert rc == ellm.OK, rc
             best_d2h = max(best_d2h, n * cb / t / 1e9)

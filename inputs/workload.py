@@ -101,11 +101,30 @@ def c1() -> Workload:
     return Workload("c1-tiny", 1, 4, 2, 64, 4, 300, seed=0, tokens_per_chunk=16, decode_headroom=64)
 
 
-def make_pool(wl: Workload, device: int, host_slots: int = 0, extra_chunks: int = 0):
+def make_pool(wl: Workload, device: int, host_slots: int = 0, extra_chunks: int = 0, extra_requests: int = 0):
     from paper_2506_15155_b200 import ellm
     nchunks = wl.batch * wl.chunks_per_request + extra_chunks
     return ellm.Pool(device, wl.n_layers, wl.hq_local, wl.hkv_local, wl.head_dim, wl.tokens_per_chunk,
-                     nchunks, nchunks, wl.batch, wl.chunks_per_request, host_slots)
+                     nchunks, nchunks, wl.batch + extra_requests, wl.chunks_per_request, host_slots)
+
+
+def fill_request(pool, wl: Workload, r: int, n: int, stream=None):
+    """Reserve n tokens for request r and append all layers' K/V (device-generated)."""
+    import torch
+    from paper_2506_15155_b200 import ellm
+    s = (stream or torch.cuda.current_stream()).cuda_stream
+    rc = pool.reserve([r], [n], s)
+    if rc != ellm.OK:
+        raise ellm.EllmError(rc, "fill reserve")
+    kb = torch.empty((n, wl.hkv_local, wl.head_dim), dtype=torch.bfloat16, device="cuda")
+    vb = torch.empty_like(kb)
+    for layer in range(wl.n_layers):
+        gen_kv_device(wl, r, 0, n, layer, 0, kb.data_ptr(), s)
+        gen_kv_device(wl, r, 0, n, layer, 1, vb.data_ptr(), s)
+        rc = pool.append(layer, [r], [n], kb, vb, s)
+        if rc != ellm.OK:
+            raise ellm.EllmError(rc, "fill append")
+    torch.cuda.synchronize()
 
 
 def gen_kv_device(wl: Workload, r: int, p0: int, n: int, layer: int, kv: int, out_ptr: int, stream=0):
