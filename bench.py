@@ -241,7 +241,7 @@ def main():
     n_steps = args.warmup + args.steps
     e2e_steps = 0 if args.no_e2e else args.steps
     UNFUSED_STEPS = 3  # comparison: separate kv_append + attention launches
-    CONC_STEPS = 10 if swap_chunks else 0  # decode steps with a concurrent swap stream
+    CONC_STEPS = 30 if swap_chunks else 0  # decode steps with a concurrent swap stream (15 per mode)
     e2e_steps += CONC_STEPS
     e2e_steps += UNFUSED_STEPS
     inputs = []
@@ -387,8 +387,13 @@ def main():
             barrier()
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s0.record(ss)
-            d0.record(stream)
+            half = CONC_STEPS // 2  # consecutive positions per mode
+            base = c_first + (0 if mode == 1 else half)
+            d0.record(stream)  # decode first (the compute stream is busy ~half*20 ms) ...
+            for s in range(base, base + half):
+                step(*inputs[s])
+            d1.record(stream)
+            s0.record(ss)      # ... then the swap work, which overlaps it on the second stream
             moved = 0
             for _ in range(3):
                 rc, slots = pool.deflate(pool.table(wl.batch)[0].tolist(), ss.cuda_stream)
@@ -397,11 +402,6 @@ def main():
                 assert rc == ellm.OK, rc
                 moved += 2 * len(slots) * pool.chunk_bytes
             s1.record(ss)
-            half = CONC_STEPS // 2  # 5 steps per mode, consecutive positions
-            base = c_first + (0 if mode == 1 else half)
-            for s in range(base, base + half):
-                step(*inputs[s])
-            d1.record(stream)
             barrier()
             swap_ms, dec_ms = s0.elapsed_time(s1), d0.elapsed_time(d1)
             conc[name] = {"decode_ms_per_step": round(dec_ms / half, 3), "swap_gbs": round(moved / swap_ms / 1e6, 2),

@@ -177,6 +177,22 @@ int ellm_deflate(ellm_pool* pool, int32_t n, const int32_t* chunk_ids, int32_t* 
  * INVALID_ARG; slot not used -> NOT_MAPPED; n > FREE KV chunks -> NO_CHUNKS. */
 int ellm_inflate(ellm_pool* pool, int32_t n, const int32_t* host_slots, int32_t* chunk_ids_out,
                  void* stream);
+/* Layer-wise pipelined offload ("offloading KV cache ... during the
+ * prefill stage", "layer-wise pipelining", "O(N) ... overhead can be completely hidden").
+ * offload_begin: reserve the lowest free host slots for the listed USED chunks (list order);
+ *   no data moves and tables still point at the chunks. Errors as deflate, plus a chunk
+ *   already being offloaded -> ALREADY_MAPPED.
+ * offload_layer: copy layer `layer`'s K/V slabs (2*Hkv*T*d*2 contiguous bytes per chunk) of the
+ *   listed chunks to their reserved slots on `stream` — call it right after that layer's
+ *   kv_append so the copy overlaps the following layers. Chunk not being offloaded ->
+ *   NOT_MAPPED. Appends into an offloading chunk after its layer was copied are not carried.
+ * offload_commit: every layer of every listed chunk copied (else INVALID_ARG): repoint the
+ *   table entries to the slots and free the chunks — the same end state (tables, slots, bytes)
+ *   as ellm_deflate of the same list. */
+int ellm_offload_begin(ellm_pool* pool, int32_t n, const int32_t* chunk_ids, int32_t* host_slots_out);
+int ellm_offload_layer(ellm_pool* pool, int32_t layer, int32_t n, const int32_t* chunk_ids, void* stream);
+int ellm_offload_commit(ellm_pool* pool, int32_t n, const int32_t* chunk_ids, void* stream);
+
 /* migrate (a8; BJ; D2D compaction): copy chunk src[i] -> dst[i], repoint the table entry,
  * src becomes FREE, dst USED. Errors: range -> OUT_OF_RANGE; any repeated id among the 2n
  * -> INVALID_ARG; src not USED KV -> NOT_MAPPED; dst ACT -> NOT_MAPPED; dst USED ->

@@ -134,6 +134,8 @@ struct Params {
   int32_t* arrivals;       // per virtual request, zero between launches
   unsigned long long* ticket;  // dynamic-unit ticket counter (monotone across launches)
   unsigned long long ticket_base;
+  const int4* dyn_info;        // per unit: {vr, tile in vr, first-segment tiles, len}, {req, 0, 0, 0}
+  const int32_t* dyn_ent;      // per unit: [U][npieces] chunk ids of its tiles (-1: none)
   const __nv_bfloat16* q;
   __nv_bfloat16* out;
   const uint4* k_new;      // fused decode append: [n][Hkv][d] new token rows, or nullptr
@@ -291,19 +293,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     int64_t t_begin = int64_t(b) * p.W_s / p.G, t_end = int64_t(b + 1) * p.W_s / p.G;
     int owner = b;
     const int32_t* cum = p.cum_s;
-    unsigned long long next_ticket = 0;
-    if (p.n_dyn > 0 && lane == 0) next_ticket = atomicAdd(p.ticket, 1ull);
+    // Dynamic units: two tickets stay outstanding (current + next), and the next unit's
+    // host-built info (first request, its tile offset / length / request id, first-segment
+    // length) and chunk entries (lane t: tile t of the unit) are loaded while the current unit
+    // streams, so switching units costs no dependent-load round trips.
+    bool dyn = false;
+    int64_t unit_start = 0;
+    int4 uinfo = make_int4(0, 0, 0, 0), uinfo2 = uinfo, ninfo = uinfo, ninfo2 = uinfo;
+    int32_t pent[8], npent[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) pent[k] = npent[k] = -1;
+    unsigned long long tk_next = 0, tk_next2 = 0;
+    if (p.n_dyn > 0 && lane == 0) {
+      tk_next = atomicAdd(p.ticket, 1ull);
+      tk_next2 = atomicAdd(p.ticket, 1ull);
+    }
     uint32_t segc = 0;  // segments started (selects the Q slot and its parity)
     for (;;) {
-      int vr = find_vr(cum, p.n_vr, t_begin);
+      int vr = dyn ? uinfo.x : find_vr(cum, p.n_vr, t_begin);
       for (int64_t tile = t_begin; tile < t_end; ++vr, ++segc) {
-        const int64_t seg_end = min(t_end, int64_t(__ldg(cum + vr + 1)));
+        const bool first_dyn_seg = dyn && tile == t_begin;  // everything known from uinfo
+        const int64_t seg_end =
+            first_dyn_seg ? min(t_end, t_begin + uinfo.z) : min(t_end, int64_t(__ldg(cum + vr + 1)));
         const int ireq = vr / p.HG, hg = vr % p.HG;
-        const int32_t len = __ldg(p.len + ireq);
-        const int32_t* trow = p.table + int64_t(__ldg(p.req + ireq)) * p.table_stride;
+        const int32_t len = first_dyn_seg ? uinfo.w : __ldg(p.len + ireq);
+        const int32_t* trow =
+            p.table + int64_t(first_dyn_seg ? uinfo2.x : __ldg(p.req + ireq)) * p.table_stride;
         // space coordinate of the request's first tile in this space, minus its tile offset
-        const int64_t tile0 = __ldg(cum + vr) -
-                              (cum == p.cum_d ? int64_t(__ldg(p.cum_s + vr + 1) - __ldg(p.cum_s + vr)) : 0);
+        const int64_t tile0 =
+            first_dyn_seg ? t_begin - uinfo.y
+                          : __ldg(cum + vr) - (dyn ? int64_t(__ldg(p.cum_s + vr + 1) - __ldg(p.cum_s + vr)) : 0);
         const int qs = int(segc % kQSlots);
         if (lane == 0) {  // stage this segment's Q rows (HB*group x D, contiguous) into its slot
           mbar_wait(qempty0 + 8 * qs, ((segc / kQSlots) & 1) ^ 1);
@@ -315,7 +334,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int64_t t = tile; t < seg_end; t += 32) {
           const int cnt = int(min(int64_t(32), seg_end - t));
           int32_t ent[8];
-          {
+          if (dyn) {  // prefetched: lane i of the unit holds the entries of the unit's tile i
+            const int src = int(t - unit_start) + lane;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) ent[k] = __shfl_sync(0xffffffffu, pent[k], src & 31);
+          } else {
             const int64_t tokb = (t + lane - tile0) * TT;  // first position of this lane's tile
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -375,13 +398,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tile = seg_end;
       }
-      // next range: the unit of the prefetched ticket (one failing ticket per CTA ends it)
+      // next range: the unit of the next ticket (two failing tickets per CTA end the phase)
       if (p.n_dyn == 0) break;
-      const int64_t u = int64_t(__shfl_sync(0xffffffffu, next_ticket, 0) - p.ticket_base);
+      const int64_t u = int64_t(__shfl_sync(0xffffffffu, tk_next, 0) - p.ticket_base);
       if (u >= p.n_dyn) break;
-      if (lane == 0) next_ticket = atomicAdd(p.ticket, 1ull);
+      const int ul = p.U * npieces;  // entries per unit
+      if (!dyn) {  // entering the dynamic phase: this unit's info was not prefetched
+        ninfo = __ldg(p.dyn_info + 2 * u);
+        ninfo2 = __ldg(p.dyn_info + 2 * u + 1);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          npent[k] = (lane < p.U && k < npieces) ? __ldg(p.dyn_ent + u * ul + lane * npieces + k) : -1;
+      }
+      uinfo = ninfo;
+      uinfo2 = ninfo2;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pent[k] = npent[k];
+      const int64_t u2 = int64_t(__shfl_sync(0xffffffffu, tk_next2, 0) - p.ticket_base);
+      if (u2 < p.n_dyn) {  // prefetch the following unit while this one streams
+        ninfo = __ldg(p.dyn_info + 2 * u2);
+        ninfo2 = __ldg(p.dyn_info + 2 * u2 + 1);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          npent[k] = (lane < p.U && k < npieces) ? __ldg(p.dyn_ent + u2 * ul + lane * npieces + k) : -1;
+      }
+      if (lane == 0) {
+        tk_next = tk_next2;
+        tk_next2 = atomicAdd(p.ticket, 1ull);
+      }
+      dyn = true;
       t_begin = u * p.U;
       t_end = min(p.W_d, t_begin + p.U);
+      unit_start = t_begin;
       owner = p.rec_dyn + int(u);
       cum = p.cum_d;
     }
@@ -648,6 +696,8 @@ cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh,
   prm.arrivals = arrivals;
   prm.ticket = plan.ticket;
   prm.ticket_base = plan.ticket_base;
+  prm.dyn_info = reinterpret_cast<const int4*>(plan.dyn_info);
+  prm.dyn_ent = plan.dyn_ent;
   prm.q = static_cast<const __nv_bfloat16*>(q);
   prm.out = static_cast<__nv_bfloat16*>(out);
   prm.k_new = static_cast<const uint4*>(plan.k_new);

@@ -90,9 +90,10 @@ cudaError_t launch_kv_append(const AppendDesc& d, int32_t n, int64_t total_rows,
                              const void* v_new, int num_sms, cudaStream_t s);
 
 // Chunk copy: dst_base + dst_idx[i]*bytes <- src_base + src_idx[i]*bytes, i < n.
+// (seg_off, seg_bytes): copy only that byte range of each chunk (seg_bytes < 0: whole chunk).
 cudaError_t launch_chunk_copy(uint8_t* dst_base, const int32_t* dst_idx, const uint8_t* src_base,
                               const int32_t* src_idx, int32_t n, int64_t chunk_bytes, int grid,
-                              cudaStream_t s);
+                              cudaStream_t s, int64_t seg_off = 0, int64_t seg_bytes = -1);
 
 struct AttnDesc {  // device-resident
   const int32_t* req;      // [n]
@@ -112,6 +113,8 @@ struct AttnPlan {
   int32_t G = 0;
   unsigned long long* ticket = nullptr;
   unsigned long long ticket_base = 0;
+  const int32_t* dyn_info = nullptr;  // device: [n_dyn][8] (int4 pairs, see attention.cu Params)
+  const int32_t* dyn_ent = nullptr;   // device: [n_dyn][U * npieces]
   // fused decode append (ellm_decode_append_attention): one new token per request, or nullptr
   const void* k_new = nullptr;
   const void* v_new = nullptr;
@@ -186,6 +189,9 @@ struct ellm_pool {
 
   // attention descriptor cache
   std::vector<int32_t> cache_key;     // req ids then lens
+  uint64_t table_epoch = 0;           // bumped by every table entry change
+  int64_t cache_info_off = 0, cache_ent_off = 0;  // dynamic-unit arrays inside the descriptor
+  uint64_t cache_epoch = ~uint64_t(0);
   const int32_t* cache_dev = nullptr;
   uint64_t cache_gen = 0;
   int32_t cache_n_vr = 0;
@@ -206,6 +212,8 @@ struct ellm_pool {
   std::vector<FreeEvent> free_events;
   std::vector<int32_t> free_event_pool;          // indices of unreferenced events
   std::vector<int32_t> chunk_ev, slot_ev;        // per chunk / host slot: event index or -1
+  // layer-wise offload in progress (ellm_offload_*): reserved slot and layers copied, per chunk
+  std::vector<int32_t> off_slot, off_layers;
 
   std::map<int32_t, std::pair<CUdeviceptr, size_t>> alias;
   int last_cuda_error = 0;

@@ -65,21 +65,24 @@ __global__ void __launch_bounds__(256) kv_append_kernel(
   }
 }
 
-// Whole-chunk copy. A warp moves one 4 KiB unit per iteration with 8 x 16 B loads in flight
-// per lane before its stores (latency hiding for HBM and for host memory over PCIe).
+// Chunk copy of bytes [seg_off, seg_off + seg_bytes) of each listed chunk (the whole chunk for
+// swap / migrate, one layer's slabs for layer-wise offload). A warp moves one 4 KiB unit per
+// iteration with 8 x 16 B loads in flight per lane before its stores (latency hiding for HBM
+// and for host memory over PCIe).
 constexpr int kCopyUnit = 4096;
 __global__ void __launch_bounds__(256) chunk_copy_kernel(uint8_t* __restrict__ dst_base,
                                                          const int32_t* __restrict__ dst_idx,
                                                          const uint8_t* __restrict__ src_base,
                                                          const int32_t* __restrict__ src_idx,
-                                                         int32_t n, int64_t chunk_bytes) {
+                                                         int32_t n, int64_t chunk_bytes, int64_t seg_off,
+                                                         int64_t seg_bytes) {
   const int lane = threadIdx.x & 31;
-  const int64_t units_per_chunk = chunk_bytes / kCopyUnit;
+  const int64_t units_per_chunk = seg_bytes / kCopyUnit;
   const int64_t total = int64_t(n) * units_per_chunk;
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
   for (int64_t w = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total; w += warps) {
     const int64_t i = w / units_per_chunk;
-    const int64_t off = (w % units_per_chunk) * kCopyUnit;
+    const int64_t off = seg_off + (w % units_per_chunk) * kCopyUnit;
     const uint4* s = reinterpret_cast<const uint4*>(src_base + int64_t(__ldg(src_idx + i)) * chunk_bytes + off);
     uint4* d = reinterpret_cast<uint4*>(dst_base + int64_t(__ldg(dst_idx + i)) * chunk_bytes + off);
     uint4 v[8];
@@ -116,13 +119,16 @@ cudaError_t launch_kv_append(const AppendDesc& d, int32_t n, int64_t total_rows,
 
 cudaError_t launch_chunk_copy(uint8_t* dst_base, const int32_t* dst_idx, const uint8_t* src_base,
                               const int32_t* src_idx, int32_t n, int64_t chunk_bytes, int grid,
-                              cudaStream_t s) {
+                              cudaStream_t s, int64_t seg_off, int64_t seg_bytes) {
   if (n <= 0) return cudaSuccess;
-  if (chunk_bytes % kCopyUnit != 0) return cudaErrorInvalidValue;
-  int64_t units = int64_t(n) * (chunk_bytes / kCopyUnit);
+  if (seg_bytes < 0) seg_bytes = chunk_bytes;
+  if (seg_bytes % kCopyUnit != 0 || seg_off % 16 != 0 || seg_off + seg_bytes > chunk_bytes)
+    return cudaErrorInvalidValue;
+  int64_t units = int64_t(n) * (seg_bytes / kCopyUnit);
   int64_t need = (units + 7) / 8;
   grid = int(std::max<int64_t>(1, std::min<int64_t>(grid, need)));
-  chunk_copy_kernel<<<grid, 256, 0, s>>>(dst_base, dst_idx, src_base, src_idx, n, chunk_bytes);
+  chunk_copy_kernel<<<grid, 256, 0, s>>>(dst_base, dst_idx, src_base, src_idx, n, chunk_bytes, seg_off,
+                                         seg_bytes);
   return cudaGetLastError();
 }
 

@@ -45,6 +45,7 @@ int32_t entry_c(const ellm_pool* p, int32_t r, int64_t i) {
 }
 void set_entry(ellm_pool* p, int32_t r, int64_t i, int32_t v) {
   entry(p, r, i) = v;
+  ++p->table_epoch;  // invalidates host-built attention descriptors (dynamic-unit entries)
   p->pending_updates.push_back(
       {int32_t(int64_t(r) * p->cfg.max_chunks_per_request + i), v});
 }
@@ -85,6 +86,31 @@ void free_host(ellm_pool* p, int64_t h) {
 }
 
 cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Copy-engine path of deflate / inflate: dst_base[dst[i]] <- src_base[src[i]], chunk_bytes each,
+// as ONE cudaMemcpyBatchAsync (host cost independent of the chunk count; copies prefer to
+// overlap with compute). Falls back to one cudaMemcpyAsync per chunk if the batch API fails.
+cudaError_t ce_copy(uint8_t* dst_base, const std::vector<int32_t>& dst, const uint8_t* src_base,
+                    const std::vector<int32_t>& src, int64_t chunk_bytes, cudaStream_t stream) {
+  const size_t n = dst.size();
+  std::vector<void*> d(n), s(n);
+  std::vector<size_t> sz(n, size_t(chunk_bytes));
+  for (size_t i = 0; i < n; ++i) {
+    d[i] = dst_base + int64_t(dst[i]) * chunk_bytes;
+    s[i] = const_cast<uint8_t*>(src_base) + int64_t(src[i]) * chunk_bytes;
+  }
+  cudaMemcpyAttributes attr;
+  std::memset(&attr, 0, sizeof(attr));
+  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+  size_t attr_idx = 0, fail_idx = 0;
+  cudaError_t e = cudaMemcpyBatchAsync(d.data(), s.data(), sz.data(), n, &attr, &attr_idx, 1, &fail_idx, stream);
+  if (e == cudaSuccess) return e;
+  cudaGetLastError();
+  for (size_t i = 0; i < n; ++i)
+    if ((e = cudaMemcpyAsync(d[i], s[i], sz[i], cudaMemcpyDefault, stream)) != cudaSuccess) return e;
+  return cudaSuccess;
+}
 
 // ---- stream-ordered reuse of freed chunks / host slots (see ellm_pool::FreeEvent) ----------
 // Record an event on `stream` after the work that frees some chunks / slots; returns its index.
@@ -231,6 +257,8 @@ int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out) {
   p->slot_idx.assign(size_t(c.host_slots), -1);
   p->chunk_ev.assign(size_t(c.max_chunks), -1);
   p->slot_ev.assign(size_t(c.host_slots), -1);
+  p->off_slot.assign(size_t(c.max_chunks), -1);
+  p->off_layers.assign(size_t(c.max_chunks), 0);
   p->table.assign(size_t(int64_t(c.max_requests) * c.max_chunks_per_request), UNMAPPED);
   p->len.assign(size_t(c.max_requests), 0);
   p->pending.assign(size_t(c.max_requests), 0);
@@ -507,25 +535,33 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
     key[size_t(i)] = reqs[i];
     key[size_t(n + i)] = int32_t(p->len[size_t(reqs[i])]);
   }
-  if (key != p->cache_key || !p->ring.still_valid(p->cache_dev, p->cache_gen)) {
+  if (key != p->cache_key || p->cache_epoch != p->table_epoch ||
+      !p->ring.still_valid(p->cache_dev, p->cache_gen)) {
     // layout: req[n] len[n] cum_s[n_vr+1] cum_d[n_vr+1] b_first[n_vr] b_last[n_vr]
-    //         u_first[n_vr] u_last[n_vr]
+    //         u_first[n_vr] u_last[n_vr] dyn_info[n_dyn][8] dyn_ent[n_dyn][U * npieces]
     std::vector<int32_t> d(size_t(2 * n + 6 * n_vr + 2));
     for (int32_t i = 0; i < n; ++i) {
       d[size_t(i)] = reqs[i];
       d[size_t(n + i)] = key[size_t(n + i)];
     }
-    int32_t* cum_s = d.data() + 2 * n;
-    int32_t* cum_d = cum_s + n_vr + 1;
+    auto tiles_of = [&](int32_t vr) { return (p->len[size_t(reqs[vr / a.HG])] + a.TT - 1) / a.TT; };
     int64_t W = 0;
-    for (int32_t vr = 0; vr < n_vr; ++vr) W += (p->len[size_t(reqs[vr / a.HG])] + a.TT - 1) / a.TT;
+    for (int32_t vr = 0; vr < n_vr; ++vr) W += tiles_of(vr);
     if (W > INT32_MAX / 2) return ELLM_ERR_UNSUPPORTED;
     // Dynamic tail only when there is enough work to balance: the last tiles(vr) / dyn_div
-    // tiles of every request go to the dynamic space.
-    const int64_t div = (p->dyn_div > 0 && W >= 4 * int64_t(p->num_sms)) ? p->dyn_div : 0;
+    // tiles of every request go to the dynamic space, in units of U <= 32 tiles (one producer
+    // lane per tile of a unit).
+    int64_t div = (p->dyn_div > 0 && W >= 4 * int64_t(p->num_sms)) ? p->dyn_div : 0;
+    if (div) {
+      int64_t wd = 0;
+      for (int32_t vr = 0; vr < n_vr; ++vr) wd += tiles_of(vr) / div;
+      if (wd == 0 || std::max<int64_t>(p->dyn_unit, (wd + kMaxDynUnits - 1) / kMaxDynUnits) > 32) div = 0;
+    }
+    int32_t* cum_s = d.data() + 2 * n;
+    int32_t* cum_d = cum_s + n_vr + 1;
     int64_t Ws = 0, Wd = 0;
     for (int32_t vr = 0; vr < n_vr; ++vr) {
-      const int64_t tiles = (p->len[size_t(reqs[vr / a.HG])] + a.TT - 1) / a.TT;
+      const int64_t tiles = tiles_of(vr);
       const int64_t dyn = div ? tiles / div : 0;  // < tiles: every request keeps >= 1 static tile
       cum_s[vr] = int32_t(Ws);
       cum_d[vr] = int32_t(Wd);
@@ -561,11 +597,46 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
         ul[vr] = -1;
       }
     }
+    // Per dynamic unit, what the producer would otherwise look up serially: the request of its
+    // first tile (+ that tile's offset in the request, the first segment's length, len, req id)
+    // and the chunk ids of all its tiles, read from the host's authoritative tables.
+    p->cache_info_off = (int64_t(d.size()) + 3) & ~int64_t(3);  // int4-aligned (16 B)
+    const int32_t tok_box = std::min(p->T, a.TT), npieces = a.TT / tok_box;
+    const int64_t U = pl.U, ulen = U * npieces;
+    p->cache_ent_off = p->cache_info_off + 8 * pl.n_dyn;
+    d.resize(size_t(p->cache_ent_off + pl.n_dyn * ulen), -1);
+    cum_s = d.data() + 2 * n;  // (resize may have moved the buffer)
+    cum_d = cum_s + n_vr + 1;
+    int32_t vr = 0;
+    for (int64_t u = 0; u < pl.n_dyn; ++u) {
+      int32_t* info = d.data() + p->cache_info_off + 8 * u;
+      int32_t* ent = d.data() + p->cache_ent_off + u * ulen;
+      for (int64_t i = 0; i < U && u * U + i < Wd; ++i) {
+        const int64_t t = u * U + i;
+        while (cum_d[vr + 1] <= t) ++vr;
+        const int32_t r = reqs[vr / a.HG];
+        const int64_t len = p->len[size_t(r)];
+        const int64_t tin = (cum_s[vr + 1] - cum_s[vr]) + (t - cum_d[vr]);  // tile within vr
+        if (i == 0) {
+          info[0] = vr;
+          info[1] = int32_t(tin);
+          info[2] = int32_t(cum_d[vr + 1] - t);
+          info[3] = int32_t(len);
+          info[4] = r;
+        }
+        for (int32_t k = 0; k < npieces; ++k) {
+          const int64_t pos = tin * a.TT + int64_t(k) * tok_box;
+          if (pos < len) ent[i * npieces + k] = entry_c(p, r, pos / p->T);
+        }
+      }
+    }
     const int32_t* dd;
     uint64_t gen;
+    if (d.size() * 4 > p->ring.seg_bytes()) return ELLM_ERR_UNSUPPORTED;
     int rc = upload_ints(p, d, S(stream), &dd, &gen);
     if (rc) return rc;
     p->cache_key = key;
+    p->cache_epoch = p->table_epoch;
     p->cache_dev = dd;
     p->cache_gen = gen;
     p->cache_n_vr = n_vr;
@@ -577,6 +648,8 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
   AttnDesc ad{dd, dd + n, cs, cs + n_vr + 1, cs + 2 * n_vr + 2, cs + 3 * n_vr + 2, cs + 4 * n_vr + 2,
               cs + 5 * n_vr + 2};
   AttnPlan plan = p->cache_plan;
+  plan.dyn_info = dd + p->cache_info_off;
+  plan.dyn_ent = dd + p->cache_ent_off;
   plan.ticket = p->d_ticket;
   plan.ticket_base = p->ticket_base;
   plan.k_new = k_new;
@@ -606,6 +679,11 @@ int ellm_release(ellm_pool* p, int32_t r, void* stream) {
   for (int64_t i = 0; i < nc; ++i) {
     int32_t e = entry_c(p, r, i);
     if (is_dev(e)) {
+      if (p->off_slot[size_t(e)] >= 0) {  // an offload in progress is abandoned with the request
+        free_host(p, p->off_slot[size_t(e)]);
+        attach_event(p, p->slot_ev, p->off_slot[size_t(e)], ev);
+        p->off_slot[size_t(e)] = -1;
+      }
       free_chunk(p, e);
       attach_event(p, p->chunk_ev, e, ev);
     }
@@ -615,6 +693,7 @@ int ellm_release(ellm_pool* p, int32_t r, void* stream) {
     }
     entry(p, r, i) = UNMAPPED;  // device mirror rows beyond len are never read
   }
+  ++p->table_epoch;
   p->len[size_t(r)] = 0;
   p->pending[size_t(r)] = 0;
   p->nonres[size_t(r)] = 0;
@@ -630,6 +709,8 @@ int ellm_deflate(ellm_pool* p, int32_t n, const int32_t* ids, int32_t* slots_out
   if (has_dup(n, ids)) return ELLM_ERR_INVALID_ARG;
   for (int32_t i = 0; i < n; ++i)
     if (p->owner[size_t(ids[i])] != KV || !p->used[size_t(ids[i])]) return ELLM_ERR_NOT_MAPPED;
+  for (int32_t i = 0; i < n; ++i)
+    if (p->off_slot[size_t(ids[i])] >= 0) return ELLM_ERR_IN_USE;  // layer-wise offload in progress
   if (n > p->cfg.host_slots - p->n_host_used) return ELLM_ERR_HOST_FULL;
   std::vector<int32_t> src(static_cast<size_t>(n)), dst(static_cast<size_t>(n));
   for (int32_t i = 0; i < n; ++i) {
@@ -651,12 +732,8 @@ int ellm_deflate(ellm_pool* p, int32_t n, const int32_t* ids, int32_t* slots_out
     if ((e = wait_freed(p, p->slot_ev, h, S(stream))) != cudaSuccess) return cuda_fail(p, e);
   uint8_t* pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
   if (p->swap_mode == 1) {
-    for (int32_t i = 0; i < n; ++i)
-      if ((e = cudaMemcpyAsync(p->host_slots + int64_t(dst[size_t(i)]) * p->chunk_bytes,
-                               pool + int64_t(src[size_t(i)]) * p->chunk_bytes,
-                               size_t(p->chunk_bytes), cudaMemcpyDeviceToHost, S(stream))) !=
-          cudaSuccess)
-        return cuda_fail(p, e);
+    if ((e = ce_copy(p->host_slots, dst, pool, src, p->chunk_bytes, S(stream))) != cudaSuccess)
+      return cuda_fail(p, e);
   } else {
     std::vector<int32_t> both(src);
     both.insert(both.end(), dst.begin(), dst.end());
@@ -708,12 +785,8 @@ int ellm_inflate(ellm_pool* p, int32_t n, const int32_t* slots, int32_t* ids_out
     if ((e = wait_freed(p, p->chunk_ev, c, S(stream))) != cudaSuccess) return cuda_fail(p, e);
   uint8_t* pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
   if (p->swap_mode == 1) {
-    for (int32_t i = 0; i < n; ++i)
-      if ((e = cudaMemcpyAsync(pool + int64_t(dst[size_t(i)]) * p->chunk_bytes,
-                               p->host_slots + int64_t(src[size_t(i)]) * p->chunk_bytes,
-                               size_t(p->chunk_bytes), cudaMemcpyHostToDevice, S(stream))) !=
-          cudaSuccess)
-        return cuda_fail(p, e);
+    if ((e = ce_copy(pool, dst, p->host_slots, src, p->chunk_bytes, S(stream))) != cudaSuccess)
+      return cuda_fail(p, e);
   } else {
     std::vector<int32_t> both(src);
     both.insert(both.end(), dst.begin(), dst.end());
@@ -736,6 +809,84 @@ int ellm_inflate(ellm_pool* p, int32_t n, const int32_t* slots, int32_t* ids_out
   return flush_table(p, S(stream));
 }
 
+// f2 — layer-wise pipelined offload during prefill. Same end state as deflate (O5).
+int ellm_offload_begin(ellm_pool* p, int32_t n, const int32_t* ids, int32_t* slots_out) {
+  if (!p || n < 0 || (n > 0 && (!ids || !slots_out))) return ELLM_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (ids[i] < 0 || ids[i] >= p->cfg.max_chunks) return ELLM_ERR_OUT_OF_RANGE;
+  if (has_dup(n, ids)) return ELLM_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (p->owner[size_t(ids[i])] != KV || !p->used[size_t(ids[i])]) return ELLM_ERR_NOT_MAPPED;
+  for (int32_t i = 0; i < n; ++i)
+    if (p->off_slot[size_t(ids[i])] >= 0) return ELLM_ERR_ALREADY_MAPPED;
+  if (n > p->cfg.host_slots - p->n_host_used) return ELLM_ERR_HOST_FULL;
+  for (int32_t i = 0; i < n; ++i) {
+    const int64_t c = ids[i], h = take_lowest_free_host(p);
+    p->slot_req[size_t(h)] = p->chunk_req[size_t(c)];
+    p->slot_idx[size_t(h)] = p->chunk_idx[size_t(c)];
+    p->off_slot[size_t(c)] = int32_t(h);
+    p->off_layers[size_t(c)] = 0;
+    slots_out[i] = int32_t(h);
+  }
+  return ELLM_OK;
+}
+
+int ellm_offload_layer(ellm_pool* p, int32_t layer, int32_t n, const int32_t* ids, void* stream) {
+  if (!p || n < 0 || (n > 0 && !ids)) return ELLM_ERR_INVALID_ARG;
+  if (layer < 0 || layer >= p->cfg.n_layers) return ELLM_ERR_OUT_OF_RANGE;
+  for (int32_t i = 0; i < n; ++i)
+    if (ids[i] < 0 || ids[i] >= p->cfg.max_chunks) return ELLM_ERR_OUT_OF_RANGE;
+  if (has_dup(n, ids)) return ELLM_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (p->off_slot[size_t(ids[i])] < 0) return ELLM_ERR_NOT_MAPPED;
+  std::vector<int32_t> both(size_t(2 * n));
+  for (int32_t i = 0; i < n; ++i) {
+    both[size_t(i)] = ids[i];
+    both[size_t(n + i)] = p->off_slot[size_t(ids[i])];
+    ++p->off_layers[size_t(ids[i])];
+  }
+  if (!p->has_dev || n == 0) return ELLM_OK;
+  cudaError_t e;
+  for (int32_t i = 0; i < n; ++i)  // the reserved slot may have been read by an inflate elsewhere
+    if ((e = wait_freed(p, p->slot_ev, both[size_t(n + i)], S(stream))) != cudaSuccess) return cuda_fail(p, e);
+  const int32_t* dd;
+  int rc = upload_ints(p, both, S(stream), &dd, nullptr);
+  if (rc) return rc;
+  uint8_t* hdev = nullptr;
+  if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&hdev), p->host_slots, 0)) != cudaSuccess)
+    return cuda_fail(p, e);
+  // layer l's K and V slabs of all local heads: [2][Hkv][T][d] bf16, contiguous in the chunk
+  const int64_t seg = int64_t(4) * p->cfg.n_heads_kv * p->T * p->cfg.head_dim;
+  if ((e = launch_chunk_copy(hdev, dd + n, static_cast<uint8_t*>(ellm_vtensor_base(p->vt)), dd, n, p->chunk_bytes,
+                             2 * p->num_sms, S(stream), int64_t(layer) * seg, seg)) != cudaSuccess)
+    return cuda_fail(p, e);
+  ++p->launches;
+  return p->ring.commit(S(stream));
+}
+
+int ellm_offload_commit(ellm_pool* p, int32_t n, const int32_t* ids, void* stream) {
+  if (!p || n < 0 || (n > 0 && !ids)) return ELLM_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (ids[i] < 0 || ids[i] >= p->cfg.max_chunks) return ELLM_ERR_OUT_OF_RANGE;
+  if (has_dup(n, ids)) return ELLM_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (p->off_slot[size_t(ids[i])] < 0) return ELLM_ERR_NOT_MAPPED;
+  for (int32_t i = 0; i < n; ++i)
+    if (p->off_layers[size_t(ids[i])] < p->cfg.n_layers) return ELLM_ERR_INVALID_ARG;
+  const int32_t ev = p->has_dev && n > 0 ? record_free_event(p, S(stream)) : -1;
+  if (p->has_dev && n > 0 && ev < 0) return ELLM_ERR_CUDA;
+  for (int32_t i = 0; i < n; ++i) {
+    const int64_t c = ids[i], h = p->off_slot[size_t(c)];
+    const int32_t r = p->chunk_req[size_t(c)], ci = p->chunk_idx[size_t(c)];
+    set_entry(p, r, ci, enc_host(h));
+    ++p->nonres[size_t(r)];
+    p->off_slot[size_t(c)] = -1;
+    free_chunk(p, c);
+    attach_event(p, p->chunk_ev, c, ev);  // free once the copies on `stream` are done
+  }
+  return flush_table(p, S(stream));
+}
+
 // a8 — O7: D2D migration (BJ north_star; the paper's own migration is ownership-only).
 int ellm_migrate(ellm_pool* p, int32_t n, const int32_t* src, const int32_t* dst, void* stream) {
   if (!p || n < 0 || (n > 0 && (!src || !dst))) return ELLM_ERR_INVALID_ARG;
@@ -748,6 +899,8 @@ int ellm_migrate(ellm_pool* p, int32_t n, const int32_t* src, const int32_t* dst
   if (has_dup(int32_t(all.size()), all.data())) return ELLM_ERR_INVALID_ARG;
   for (int32_t i = 0; i < n; ++i)
     if (p->owner[size_t(src[i])] != KV || !p->used[size_t(src[i])]) return ELLM_ERR_NOT_MAPPED;
+  for (int32_t i = 0; i < n; ++i)
+    if (p->off_slot[size_t(src[i])] >= 0) return ELLM_ERR_IN_USE;  // layer-wise offload in progress
   for (int32_t i = 0; i < n; ++i) {
     if (p->owner[size_t(dst[i])] != KV) return ELLM_ERR_NOT_MAPPED;
     if (p->used[size_t(dst[i])]) return ELLM_ERR_ALREADY_MAPPED;

@@ -68,6 +68,9 @@ _SIGS = {
     "ellm_deflate": (ctypes.c_int, [_P, _I32, _P, _P, _V]),
     "ellm_inflate": (ctypes.c_int, [_P, _I32, _P, _P, _V]),
     "ellm_migrate": (ctypes.c_int, [_P, _I32, _P, _P, _V]),
+    "ellm_offload_begin": (ctypes.c_int, [_P, _I32, _P, _P]),
+    "ellm_offload_layer": (ctypes.c_int, [_P, _I32, _I32, _P, _V]),
+    "ellm_offload_commit": (ctypes.c_int, [_P, _I32, _P, _V]),
     "ellm_pool_grow": (ctypes.c_int, [_P, _I64]),
     "ellm_pool_shrink": (ctypes.c_int, [_P, _I64]),
     "ellm_set_swap_mode": (ctypes.c_int, [_P, _I32]),
@@ -191,6 +194,20 @@ class Pool:
         out = np.full(len(a), -1, np.int32)
         rc = ellm_inflate(self._h, len(a), _ptr(a), _ptr(out), _sptr(stream))
         return rc, out
+
+    def offload_begin(self, ids):
+        a = _i32(ids)
+        out = np.full(len(a), -1, np.int32)
+        rc = ellm_offload_begin(self._h, len(a), _ptr(a), _ptr(out))
+        return rc, out
+
+    def offload_layer(self, layer, ids, stream=None) -> int:
+        a = _i32(ids)
+        return ellm_offload_layer(self._h, int(layer), len(a), _ptr(a), _sptr(stream))
+
+    def offload_commit(self, ids, stream=None) -> int:
+        a = _i32(ids)
+        return ellm_offload_commit(self._h, len(a), _ptr(a), _sptr(stream))
 
     def migrate(self, src, dst, stream=None) -> int:
         s, d = _i32(src), _i32(dst)
