@@ -662,7 +662,8 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
                                          p->d_part_ml, p->d_arrivals, scale, S(stream), &launches);
   p->launches += launches;
   if (e != cudaSuccess) return cuda_fail(p, e);
-  if (plan.n_dyn > 0) p->ticket_base += uint64_t(plan.n_dyn) + uint64_t(plan.G);  // tickets consumed
+  // tickets consumed: every unit once, plus the two outstanding tickets each CTA ends with
+  if (plan.n_dyn > 0) p->ticket_base += uint64_t(plan.n_dyn) + 2 * uint64_t(plan.G);
   return p->ring.commit(S(stream));
 }
 
