@@ -435,6 +435,33 @@ def main():
     assert pool.grow(n_vmm) == ellm.OK
     t_grow = time.perf_counter() - t0
     st1 = pool.stats()
+
+    # ---- f1: the caller-side cost of shrink / grow of one default map unit while a
+    #      decode step's attention launches are still queued on the GPU — device-synchronising
+    #      unmap + on-demand map, vs asynchronous unmapping + speculative pre-mapping ----
+    k_unit = max(1, (64 << 20) // pool.chunk_bytes)
+
+    def vmm_timed(fn):
+        for l in range(L):
+            pool.attention(l, reqs, inputs[0][0][l], out[l], scale, sp)
+        s_before = pool.stats()
+        t0 = time.perf_counter()
+        assert fn() == ellm.OK
+        dt = time.perf_counter() - t0
+        s_after = pool.stats()
+        torch.cuda.synchronize()
+        assert pool.vmm_sync() == ellm.OK
+        return {"host_ms": round(dt * 1e3, 3), "crit_vmm_ms": round((s_after["crit_vmm_ns"] - s_before["crit_vmm_ns"]) / 1e6, 3),
+                "maps": s_after["n_map"] - s_before["n_map"], "unmaps": s_after["n_unmap"] - s_before["n_unmap"]}
+
+    f1 = {"chunks": k_unit, "gpu_queue": f"{L} attention launches (~{ms_step:.0f} ms) queued before each call"}
+    f1["sync"] = {"shrink": vmm_timed(lambda: pool.shrink(k_unit)), "grow": vmm_timed(lambda: pool.grow(k_unit))}
+    assert pool.set_vmm_overlap(64 << 20, True) == ellm.OK and pool.vmm_sync() == ellm.OK
+    f1["overlap"] = {"shrink": vmm_timed(lambda: pool.shrink(k_unit)), "grow": vmm_timed(lambda: pool.grow(k_unit)),
+                     "premap_hits": pool.stats()["premap_hits"]}
+    assert pool.set_vmm_overlap(0, False) == ellm.OK and pool.vmm_sync() == ellm.OK
+    torch.cuda.synchronize()
+
     rows = {
         "a1_pool_create": {"s": round(t_create, 3), "chunks_mapped": st_create["n_map"],
                            "map_us_per_chunk": round(st_create["map_ns"] / max(1, st_create["n_map"]) / 1e3, 2),
@@ -448,6 +475,7 @@ def main():
         "a9_pool_shrink_grow": {"chunks": n_vmm, "shrink_ms": round(t_shrink * 1e3, 2), "grow_ms": round(t_grow * 1e3, 2),
                                 "unmap_us_per_chunk": round((st1["unmap_ns"] - st0["unmap_ns"]) / max(1, n_vmm) / 1e3, 2),
                                 "map_us_per_chunk": round((st1["map_ns"] - st0["map_ns"]) / max(1, n_vmm) / 1e3, 2)},
+        "f1_vmm_overlap": f1,
     }
 
     cpu = None

@@ -98,6 +98,13 @@ typedef struct {
   int64_t map_ns, unmap_ns;        /* host wall time spent in them */
   int64_t chunk_bytes;             /* bytes per chunk */
   int64_t mapped_bytes;            /* physical device bytes currently mapped */
+  /* f1 (ellm_set_vmm_overlap) */
+  int64_t premapped_bytes;         /* all-ACT units mapped ahead of pool_grow (premap window) */
+  int64_t pending_unmap;           /* all-ACT units still mapped, waiting for the async unmap */
+  int64_t crit_vmm_ns;             /* VMM + device-sync wall time inside pool_grow / pool_shrink
+                                      (the caller's critical path; worker time is excluded) */
+  int64_t n_steal;                 /* units pool_grow backed with a pending-unmap unit's handle */
+  int64_t premap_hits;             /* units pool_grow found already mapped while all-ACT */
 } ellm_stats;
 
 /* ---- vtensor (VMM) ------------------------------------------------------------------
@@ -206,6 +213,26 @@ int ellm_migrate(ellm_pool* pool, int32_t n, const int32_t* src, const int32_t* 
  * n > #FREE KV -> IN_USE. */
 int ellm_pool_grow(ellm_pool* pool, int64_t n);
 int ellm_pool_shrink(ellm_pool* pool, int64_t n);
+
+/* VMM-overhead hiding. Off by default; the first call starts one
+ * background worker thread per pool. Ownership, tables and every other result are unchanged —
+ * only WHEN physical memory is mapped / unmapped moves off the caller's thread.
+ *   premap_bytes ("decoding speculative pre-mapping"): keep the lowest all-ACT map
+ *     units covering premap_bytes (rounded up to whole units) physically mapped, so pool_grow of
+ *     the next ACT ids makes no driver call; the worker refills the window after each grow.
+ *     The paper's budget is < 50 MB; a map unit is >= 64 MiB by default (config).
+ *   async_unmap = 1 ("asynchronous unmapping"): pool_shrink only changes ownership;
+ *     the worker device-synchronises and unmaps + releases units left all-ACT. A pool_grow that
+ *     needs fresh memory while such a unit is still mapped maps that unit's physical handle at
+ *     the new address instead (one handle, two mappings until the old one is unmapped —
+ *     invariant I2 relaxed as S:205 allows); pending work on the memory is ordered through the
+ *     donor chunks' free events. pool_grow of a unit still awaiting unmap reuses it as is.
+ * Device-synchronising calls from the worker thread: do not run it during stream capture.
+ * ellm_vmm_sync waits until the worker is idle and returns its sticky error (ELLM_ERR_CUDA)
+ * or ELLM_OK. NO_DEVICE on a host-only pool; INVALID_ARG for premap_bytes < 0 or
+ * async_unmap not in {0,1}. */
+int ellm_set_vmm_overlap(ellm_pool* pool, int64_t premap_bytes, int32_t async_unmap);
+int ellm_vmm_sync(ellm_pool* pool);
 
 /* Swap engine selection: 0 = SM copy kernels (default), 1 = DMA copy engines
  * (cudaMemcpyAsync per chunk). Both are exact byte copies. */

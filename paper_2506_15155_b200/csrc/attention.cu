@@ -159,7 +159,7 @@ constexpr int kFirst = 1, kLast = 2, kDone = 4;  // stage metadata flags
 // are lane-parallel reductions, each record's weight is broadcast by shuffle, and a record's o
 // row is one coalesced D*4-byte load across the row's lanes. Records written by other SMs are
 // read through L2 (__ldcg): L1 is not coherent across SMs.
-template <int D>
+template <int D, int DEPTH>  // DEPTH: record loads in flight per lane (register cost 5*DEPTH)
 __device__ __forceinline__ void merge_request(const Params& p, int vr, int rows, int nsub, int HB, int w0,
                                               int nw) {  // run by warps [w0, w0 + nw)
   constexpr int LPR = D / 4;         // lanes per row
@@ -194,15 +194,24 @@ __device__ __forceinline__ void merge_request(const Params& p, int vr, int rows,
         L += my_w * ml.y;
       }
       const int cnt = int(min(int64_t(LPR), P - base));
-#pragma unroll 4
-      for (int j = 0; j < cnt; ++j) {
-        const float w = __shfl_sync(seg_mask, my_w, j, LPR);
-        if (live) {
-          const float4 o = __ldcg(reinterpret_cast<const float4*>(p.part + (pid(base + j) * rows + row) * D) + e4);
-          acc.x += w * o.x;
-          acc.y += w * o.y;
-          acc.z += w * o.z;
-          acc.w += w * o.w;
+      for (int j0 = 0; j0 < cnt; j0 += DEPTH) {  // DEPTH independent record loads in flight
+        float4 ov[DEPTH];
+        float wv[DEPTH];
+#pragma unroll
+        for (int jj = 0; jj < DEPTH; ++jj) {
+          const int j = j0 + jj;
+          wv[jj] = __shfl_sync(seg_mask, my_w, j & (LPR - 1), LPR);  // 0 for lanes past P
+          ov[jj] = (live && j < cnt)
+                       ? __ldcg(reinterpret_cast<const float4*>(p.part + (pid(base + j) * rows + row) * D) + e4)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int jj = 0; jj < DEPTH; ++jj) {
+          const float w = (j0 + jj < cnt) ? wv[jj] : 0.f;
+          acc.x += w * ov[jj].x;
+          acc.y += w * ov[jj].y;
+          acc.z += w * ov[jj].z;
+          acc.w += w * ov[jj].w;
         }
       }
     }
@@ -311,10 +320,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t segc = 0;  // segments started (selects the Q slot and its parity)
     for (;;) {
       int vr = dyn ? uinfo.x : find_vr(cum, p.n_vr, t_begin);
-      for (int64_t tile = t_begin; tile < t_end; ++vr, ++segc) {
+      for (int64_t tile = t_begin; tile < t_end; ++vr) {
         const bool first_dyn_seg = dyn && tile == t_begin;  // everything known from uinfo
         const int64_t seg_end =
             first_dyn_seg ? min(t_end, t_begin + uinfo.z) : min(t_end, int64_t(__ldg(cum + vr + 1)));
+        // a request with no tiles in this space (a short request's empty dynamic tail) is not a
+        // segment: staging its Q would leave a Q slot no consumer releases
+        if (seg_end <= tile) continue;
         const int ireq = vr / p.HG, hg = vr % p.HG;
         const int32_t len = first_dyn_seg ? uinfo.w : __ldg(p.len + ireq);
         const int32_t* trow =
@@ -397,6 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         tile = seg_end;
+        ++segc;
       }
       // next range: the unit of the next ticket (two failing tickets per CTA end the phase)
       if (p.n_dyn == 0) break;
@@ -620,13 +633,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           else now = 1;        // deferred list full: warp 0 merges this one right away
         }
       }
-      if (__shfl_sync(0xffffffffu, now, 0)) merge_request<D>(p, vr, rows, NSUB, HB, 0, 1);
+      if (__shfl_sync(0xffffffffu, now, 0)) merge_request<D, 1>(p, vr, rows, NSUB, HB, 0, 1);
     }
   }
   // ---- end of this CTA's work: all consumer warps merge the requests it completed ----
   asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
   __threadfence();
-  for (int k = 0; k < s_n_merge; ++k) merge_request<D>(p, s_merge[k], rows, NSUB, HB, 0, kConsumerWarps);
+  for (int k = 0; k < s_n_merge; ++k) merge_request<D, 8>(p, s_merge[k], rows, NSUB, HB, 0, kConsumerWarps);
 }
 
 template <int D, int HB>

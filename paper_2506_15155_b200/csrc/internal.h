@@ -4,11 +4,16 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <condition_variable>
 #include <cstdint>
 #include <map>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/ellm.h"
+
+struct ellm_vtensor;
 
 namespace ellm {
 
@@ -33,6 +38,8 @@ struct Driver {
 const Driver& driver();  // loads once; .ok false if unavailable
 
 int64_t now_ns();
+int vt_unmap_slot_nosync(ellm_vtensor* vt, int64_t slot);
+int vt_map_from(ellm_vtensor* vt, int64_t dst, int64_t src);
 
 // ---- staging ring: host-snapshot -> device small-array uploads, stream-ordered ----------
 // Pinned host + device buffers split into segments; a segment is reused only after the
@@ -146,6 +153,7 @@ struct ellm_vtensor {
   CUdeviceptr base = 0;
   std::vector<CUmemGenericAllocationHandle> handles;
   std::vector<uint8_t> mapped;
+  std::vector<uint8_t> owned;  // slot owns (releases) its handle; 0 after vt_map_from moved it
   int64_t n_map = 0, n_unmap = 0, map_ns = 0, unmap_ns = 0;
 };
 
@@ -214,6 +222,24 @@ struct ellm_pool {
   std::vector<int32_t> chunk_ev, slot_ev;        // per chunk / host slot: event index or -1
   // layer-wise offload in progress (ellm_offload_*): reserved slot and layers copied, per chunk
   std::vector<int32_t> off_slot, off_layers;
+
+  // f1: VMM work off the caller's critical path. A worker thread keeps
+  // the `premap_units` lowest all-ACT units mapped ahead of pool_grow (speculative pre-mapping)
+  // and unmaps units pool_shrink left all-ACT (asynchronous unmapping). pool_grow that needs an
+  // unmapped unit while another awaits its async unmap takes that unit's physical handle
+  // (multi-mapping); the donor's VA stays mapped ("doomed") until the worker unmaps it.
+  std::mutex vmm_mu;                 // guards vt, unit_kv, doomed and the fields below
+  std::condition_variable vmm_cv;
+  std::thread vmm_thread;
+  bool vmm_started = false, vmm_stop = false, vmm_dirty = false, vmm_busy = false;
+  int64_t premap_units = 0;
+  bool async_unmap = false;
+  int64_t vmm_delay_us = 0;          // test knob (ELLM_VMM_WORKER_DELAY_US): worker start delay
+  std::vector<uint8_t> doomed;       // per unit: handle moved away, VA mapping awaits unmap
+  std::vector<uint64_t> unit_gen;    // per unit: bumped when its first chunk becomes KV
+  int vmm_error = 0;                 // sticky worker failure, reported by ellm_vmm_sync
+  int64_t crit_vmm_ns = 0;           // VMM + device-sync time inside pool_grow / pool_shrink
+  int64_t n_steal = 0, premap_hits = 0;
 
   std::map<int32_t, std::pair<CUdeviceptr, size_t>> alias;
   int last_cuda_error = 0;

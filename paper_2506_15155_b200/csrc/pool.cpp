@@ -6,6 +6,7 @@
 // Every entry point validates all preconditions before mutating (include/ellm.h
 // "Conventions"); allocation is lowest-id-first (R7).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <cstdlib>
@@ -188,6 +189,68 @@ int upload_ints(ellm_pool* p, const std::vector<int32_t>& v, cudaStream_t stream
   return ELLM_OK;
 }
 
+// ---- f1: VMM overlap (see ellm_pool) — the *_units helpers run with vmm_mu held -----------
+// Units that should be mapped: every unit holding a KV chunk, plus the premap window (the
+// premap_units lowest all-ACT units: pool_grow takes the lowest ACT ids next).
+std::vector<uint8_t> wanted_units(const ellm_pool* p) {
+  std::vector<uint8_t> w(p->unit_kv.size(), 0);
+  int64_t k = 0;
+  for (size_t u = 0; u < w.size(); ++u)
+    if (p->unit_kv[u] > 0) w[u] = 1;
+    else if (k < p->premap_units) w[u] = 1, ++k;
+  return w;
+}
+
+void vmm_kick(ellm_pool* p) {  // called with vmm_mu held
+  if (!p->vmm_started) return;
+  p->vmm_dirty = true;
+  p->vmm_cv.notify_all();
+}
+
+// Worker: unmap doomed / unwanted units (after a device sync, so work enqueued before their
+// chunks became ACT has finished), then map the premap window. Each driver call runs with
+// vmm_mu held, so pool_grow / pool_shrink see consistent unit state.
+void vmm_worker(ellm_pool* p) {
+  cudaSetDevice(p->cfg.device);
+  std::unique_lock<std::mutex> lk(p->vmm_mu);
+  for (;;) {
+    p->vmm_cv.wait(lk, [&] { return p->vmm_stop || p->vmm_dirty; });
+    if (p->vmm_stop) break;
+    p->vmm_dirty = false;
+    p->vmm_busy = true;
+    if (p->vmm_delay_us > 0) {
+      lk.unlock();
+      std::this_thread::sleep_for(std::chrono::microseconds(p->vmm_delay_us));
+      lk.lock();
+    }
+    std::vector<uint8_t> want = wanted_units(p);
+    std::vector<std::pair<int64_t, uint64_t>> cand;  // (unit, generation) before the sync
+    for (size_t u = 0; u < want.size(); ++u)
+      if (p->vt->mapped[u] && p->unit_kv[u] == 0 && (p->doomed[u] || !want[u]))
+        cand.push_back({int64_t(u), p->unit_gen[u]});
+    if (!cand.empty()) {
+      lk.unlock();
+      const cudaError_t e = cudaDeviceSynchronize();
+      lk.lock();
+      if (e != cudaSuccess) p->vmm_error = ELLM_ERR_CUDA;
+      want = wanted_units(p);
+      for (auto [u, gen] : cand) {  // re-check: a grow may have taken the unit back meanwhile
+        if (e != cudaSuccess || !p->vt->mapped[size_t(u)] || p->unit_kv[size_t(u)] != 0 ||
+            p->unit_gen[size_t(u)] != gen || !(p->doomed[size_t(u)] || !want[size_t(u)]))
+          continue;
+        if (vt_unmap_slot_nosync(p->vt, u) != ELLM_OK) p->vmm_error = ELLM_ERR_CUDA;
+        p->doomed[size_t(u)] = 0;
+      }
+    }
+    want = wanted_units(p);
+    for (size_t u = 0; u < want.size() && !p->vmm_stop; ++u)
+      if (want[u] && !p->vt->mapped[u] && ellm_vtensor_map(p->vt, int64_t(u), 1) != ELLM_OK)
+        p->vmm_error = ELLM_ERR_CUDA;
+    p->vmm_busy = false;
+    p->vmm_cv.notify_all();
+  }
+}
+
 bool check_reqs_range(const ellm_pool* p, int32_t n, const int32_t* r) {
   for (int32_t i = 0; i < n; ++i)
     if (r[i] < 0 || r[i] >= p->cfg.max_requests) return false;
@@ -300,6 +363,9 @@ int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out) {
   int64_t n_units = (c.max_chunks + p->chunks_per_unit - 1) / p->chunks_per_unit;
   if ((rc = ellm_vtensor_create(c.device, size_t(p->unit_bytes), n_units, &p->vt))) return fail(rc);
   p->unit_kv.assign(size_t(n_units), 0);
+  p->unit_gen.assign(size_t(n_units), 0);
+  p->doomed.assign(size_t(n_units), 0);
+  if (const char* v = std::getenv("ELLM_VMM_WORKER_DELAY_US")) p->vmm_delay_us = std::max(0L, std::atol(v));
   for (int64_t i = 0; i < c.initial_chunks; ++i) ++p->unit_kv[size_t(i / p->chunks_per_unit)];
   for (int64_t u = 0; u < n_units;) {  // map runs of units that hold KV chunks
     int64_t v = u;
@@ -354,6 +420,14 @@ int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out) {
 
 int ellm_pool_destroy(ellm_pool* p) {
   if (!p) return ELLM_ERR_INVALID_ARG;
+  if (p->vmm_started) {
+    {
+      std::lock_guard<std::mutex> g(p->vmm_mu);
+      p->vmm_stop = true;
+    }
+    p->vmm_cv.notify_all();
+    p->vmm_thread.join();
+  }
   if (p->has_dev) {
     cudaSetDevice(p->cfg.device);
     cudaDeviceSynchronize();
@@ -379,6 +453,7 @@ int ellm_pool_destroy(ellm_pool* p) {
 
 int ellm_pool_stats(const ellm_pool* p, ellm_stats* o) {
   if (!p || !o) return ELLM_ERR_INVALID_ARG;
+  std::lock_guard<std::mutex> g(const_cast<ellm_pool*>(p)->vmm_mu);
   o->kv_free = p->n_free_kv;
   o->kv_used = p->n_used_kv;
   o->act = p->n_act;
@@ -393,6 +468,18 @@ int ellm_pool_stats(const ellm_pool* p, ellm_stats* o) {
   if (p->vt)
     for (uint8_t m : p->vt->mapped) mapped += m;
   o->mapped_bytes = mapped * p->unit_bytes;
+  o->premapped_bytes = o->pending_unmap = 0;
+  if (p->vt) {
+    const std::vector<uint8_t> want = wanted_units(p);
+    for (size_t u = 0; u < want.size(); ++u)
+      if (p->vt->mapped[u] && p->unit_kv[u] == 0) {
+        if (p->doomed[u] || !want[u]) ++o->pending_unmap;
+        else o->premapped_bytes += p->unit_bytes;
+      }
+  }
+  o->crit_vmm_ns = p->crit_vmm_ns;
+  o->n_steal = p->n_steal;
+  o->premap_hits = p->premap_hits;
   return ELLM_OK;
 }
 
@@ -937,39 +1024,84 @@ int ellm_migrate(ellm_pool* p, int32_t n, const int32_t* src, const int32_t* dst
 }
 
 // a9 — inflation (3)-(4): ACT -> KV ownership transfer + on-demand remap.
+// With f1 enabled the units it needs are usually pre-mapped already (no VMM call here); an
+// unmapped one takes the physical handle of a unit awaiting async unmap when there is one.
 int ellm_pool_grow(ellm_pool* p, int64_t n) {
   if (!p || n < 0) return ELLM_ERR_INVALID_ARG;
   if (n > p->n_act) return ELLM_ERR_NO_CHUNKS;
   std::vector<int64_t> ids;
   for (int64_t c = 0; c < p->cfg.max_chunks && int64_t(ids.size()) < n; ++c)
     if (p->owner[size_t(c)] == ACT) ids.push_back(c);
+  std::unique_lock<std::mutex> lk(p->vmm_mu, std::defer_lock);
   if (p->has_dev) {  // map first so a driver failure leaves ownership unchanged
-    std::set<int64_t> units;
-    for (int64_t c : ids)
-      if (!p->vt->mapped[size_t(c / p->chunks_per_unit)]) units.insert(c / p->chunks_per_unit);
-    for (auto it = units.begin(); it != units.end();) {  // map contiguous runs at once
-      int64_t u0 = *it, u1 = u0 + 1;
-      for (++it; it != units.end() && *it == u1; ++it) ++u1;
-      int rc = ellm_vtensor_map(p->vt, u0, u1 - u0);
-      if (rc) return rc;
+    lk.lock();
+    const int64_t t0 = now_ns();
+    std::set<int64_t> units, need;
+    for (int64_t c : ids) units.insert(c / p->chunks_per_unit);
+    for (int64_t u : units)
+      if (!p->vt->mapped[size_t(u)] || p->doomed[size_t(u)]) need.insert(u);
+      else if (p->unit_kv[size_t(u)] == 0) ++p->premap_hits;
+    bool synced = false;
+    std::vector<int64_t> fresh;  // units mapped with new physical memory
+    for (int64_t u : need) {
+      if (p->doomed[size_t(u)]) {  // its old VA mapping must go before it is reused
+        if (!synced && cudaDeviceSynchronize() != cudaSuccess) return ELLM_ERR_CUDA;
+        synced = true;
+        if (int rc = vt_unmap_slot_nosync(p->vt, u)) return rc;
+        p->doomed[size_t(u)] = 0;
+      }
+      int64_t donor = -1;  // a mapped all-ACT unit outside the premap window: awaiting unmap
+      if (p->async_unmap) {
+        const std::vector<uint8_t> want = wanted_units(p);
+        for (int64_t v = int64_t(p->unit_kv.size()) - 1; v >= 0 && donor < 0; --v)
+          if (p->vt->mapped[size_t(v)] && !p->doomed[size_t(v)] && p->unit_kv[size_t(v)] == 0 &&
+              !want[size_t(v)] && !units.count(v))
+            donor = v;
+      }
+      if (donor >= 0) {
+        if (int rc = vt_map_from(p->vt, u, donor)) return rc;
+        p->doomed[size_t(donor)] = 1;
+        ++p->n_steal;
+        // the memory's pending users are those of the donor's chunks: carry their free events
+        for (int64_t k = 0; k < p->chunks_per_unit; ++k) {
+          const int64_t cu = u * p->chunks_per_unit + k, cv = donor * p->chunks_per_unit + k;
+          if (cu < p->cfg.max_chunks && cv < p->cfg.max_chunks)
+            attach_event(p, p->chunk_ev, cu, p->chunk_ev[size_t(cv)]);
+        }
+      } else {
+        fresh.push_back(u);
+      }
     }
+    for (size_t i = 0; i < fresh.size();) {  // map contiguous runs at once
+      size_t k = i + 1;
+      while (k < fresh.size() && fresh[k] == fresh[k - 1] + 1) ++k;
+      if (int rc = ellm_vtensor_map(p->vt, fresh[i], int64_t(k - i))) return rc;
+      i = k;
+    }
+    p->crit_vmm_ns += now_ns() - t0;
   }
   for (int64_t c : ids) {
     p->owner[size_t(c)] = KV;
     p->used[size_t(c)] = 0;
-    if (p->has_dev) ++p->unit_kv[size_t(c / p->chunks_per_unit)];
+    if (p->has_dev && p->unit_kv[size_t(c / p->chunks_per_unit)]++ == 0)
+      ++p->unit_gen[size_t(c / p->chunks_per_unit)];
     ++p->n_free_kv;
     --p->n_act;
     p->free_hint = std::min(p->free_hint, c);
   }
+  if (p->has_dev) vmm_kick(p);  // refill the premap window
   return ELLM_OK;
 }
 
 // a9 — deflation, "the reverse process": highest-id FREE KV chunks -> ACT, and
-// physical memory whose chunks are all ACT is unmapped.
+// physical memory whose chunks are all ACT is unmapped — here, device-synchronising,
+// unless f1's asynchronous unmapping hands it to the worker; units inside the premap window
+// stay mapped either way.
 int ellm_pool_shrink(ellm_pool* p, int64_t n) {
   if (!p || n < 0) return ELLM_ERR_INVALID_ARG;
   if (n > p->n_free_kv) return ELLM_ERR_IN_USE;
+  std::unique_lock<std::mutex> lk(p->vmm_mu, std::defer_lock);
+  if (p->has_dev) lk.lock();
   std::vector<int64_t> units;
   for (int64_t c = p->cfg.max_chunks - 1; c >= 0 && n > 0; --c)
     if (p->owner[size_t(c)] == KV && !p->used[size_t(c)]) {
@@ -980,17 +1112,46 @@ int ellm_pool_shrink(ellm_pool* p, int64_t n) {
       int64_t u = c / p->chunks_per_unit;
       if (p->has_dev && --p->unit_kv[size_t(u)] == 0) units.push_back(u);
     }
-  if (p->has_dev) {  // unmap contiguous runs at once (one device sync per run)
+  if (!p->has_dev) return ELLM_OK;
+  if (!p->async_unmap && !units.empty()) {
+    const int64_t t0 = now_ns();
+    const std::vector<uint8_t> want = wanted_units(p);
     std::sort(units.begin(), units.end());
-    for (size_t i = 0; i < units.size();) {
-      size_t k = i + 1;
-      while (k < units.size() && units[k] == units[k - 1] + 1) ++k;
-      int rc = ellm_vtensor_unmap(p->vt, units[i], int64_t(k - i));
-      if (rc) return rc;
-      i = k;
+    bool synced = false;
+    for (int64_t u : units)
+      if (!want[size_t(u)] && p->vt->mapped[size_t(u)]) {
+        if (!synced && cudaDeviceSynchronize() != cudaSuccess) return ELLM_ERR_CUDA;
+        synced = true;
+        if (int rc = vt_unmap_slot_nosync(p->vt, u)) return rc;
+      }
+    p->crit_vmm_ns += now_ns() - t0;
+  }
+  vmm_kick(p);
+  return ELLM_OK;
+}
+
+int ellm_set_vmm_overlap(ellm_pool* p, int64_t premap_bytes, int32_t async_unmap) {
+  if (!p || premap_bytes < 0 || (async_unmap != 0 && async_unmap != 1)) return ELLM_ERR_INVALID_ARG;
+  if (!p->has_dev) return ELLM_ERR_NO_DEVICE;
+  {
+    std::lock_guard<std::mutex> g(p->vmm_mu);
+    p->premap_units = (premap_bytes + p->unit_bytes - 1) / p->unit_bytes;
+    p->async_unmap = async_unmap != 0;
+    if (!p->vmm_started) {
+      p->vmm_thread = std::thread(vmm_worker, p);
+      p->vmm_started = true;
     }
+    vmm_kick(p);
   }
   return ELLM_OK;
+}
+
+int ellm_vmm_sync(ellm_pool* p) {
+  if (!p) return ELLM_ERR_INVALID_ARG;
+  if (!p->has_dev || !p->vmm_started) return ELLM_OK;
+  std::unique_lock<std::mutex> lk(p->vmm_mu);
+  p->vmm_cv.wait(lk, [&] { return !p->vmm_dirty && !p->vmm_busy; });
+  return p->vmm_error;
 }
 
 int ellm_get_table(const ellm_pool* p, int32_t r, int32_t* entries, int32_t cap, int32_t* n_out,

@@ -197,6 +197,7 @@ int ellm_vtensor_create(int32_t device, size_t slot_bytes, int64_t n_slots, ellm
   }
   vt->handles.assign(size_t(n_slots), 0);
   vt->mapped.assign(size_t(n_slots), 0);
+  vt->owned.assign(size_t(n_slots), 0);
   *out = vt;
   return ELLM_OK;
 }
@@ -242,7 +243,7 @@ int ellm_vtensor_map(ellm_vtensor* vt, int64_t first, int64_t n) {
     undo(first + n);
     return ELLM_ERR_CUDA;
   }
-  for (int64_t i = first; i < first + n; ++i) vt->mapped[size_t(i)] = 1;
+  for (int64_t i = first; i < first + n; ++i) vt->mapped[size_t(i)] = vt->owned[size_t(i)] = 1;
   vt->n_map += n;
   vt->map_ns += now_ns() - t0;
   return ELLM_OK;
@@ -262,14 +263,64 @@ int ellm_vtensor_unmap(ellm_vtensor* vt, int64_t first, int64_t n) {
   for (int64_t i = first; i < first + n; ++i) {
     CUdeviceptr va = vt->base + CUdeviceptr(i) * vt->slot_bytes;
     if (d.memUnmap(va, vt->slot_bytes) != CUDA_SUCCESS) return ELLM_ERR_CUDA;
-    if (d.memRelease(vt->handles[size_t(i)]) != CUDA_SUCCESS) return ELLM_ERR_CUDA;
+    if (vt->owned[size_t(i)] && d.memRelease(vt->handles[size_t(i)]) != CUDA_SUCCESS) return ELLM_ERR_CUDA;
     vt->handles[size_t(i)] = 0;
-    vt->mapped[size_t(i)] = 0;
+    vt->mapped[size_t(i)] = vt->owned[size_t(i)] = 0;
     ++vt->n_unmap;
   }
   vt->unmap_ns += now_ns() - t0;
   return ELLM_OK;
 }
+
+}  // extern "C"
+
+namespace ellm {
+
+// Unmap one slot without synchronising the device (the caller guarantees no pending work can
+// touch it); its physical handle is released only if this slot still owns it.
+int vt_unmap_slot_nosync(ellm_vtensor* vt, int64_t slot) {
+  if (!vt->mapped[size_t(slot)]) return ELLM_ERR_NOT_MAPPED;
+  const Driver& d = driver();
+  int64_t t0 = now_ns();
+  if (d.memUnmap(vt->base + CUdeviceptr(slot) * vt->slot_bytes, vt->slot_bytes) != CUDA_SUCCESS)
+    return ELLM_ERR_CUDA;
+  if (vt->owned[size_t(slot)] && d.memRelease(vt->handles[size_t(slot)]) != CUDA_SUCCESS) return ELLM_ERR_CUDA;
+  vt->handles[size_t(slot)] = 0;
+  vt->mapped[size_t(slot)] = vt->owned[size_t(slot)] = 0;
+  ++vt->n_unmap;
+  vt->unmap_ns += now_ns() - t0;
+  return ELLM_OK;
+}
+
+// Multi-mapping: map the physical handle behind slot `src` also at slot `dst` and move
+// its ownership to dst; src keeps a VA mapping of the same memory until it is unmapped (async).
+int vt_map_from(ellm_vtensor* vt, int64_t dst, int64_t src) {
+  if (vt->mapped[size_t(dst)]) return ELLM_ERR_ALREADY_MAPPED;
+  if (!vt->mapped[size_t(src)] || !vt->owned[size_t(src)]) return ELLM_ERR_NOT_MAPPED;
+  const Driver& d = driver();
+  int64_t t0 = now_ns();
+  const CUdeviceptr va = vt->base + CUdeviceptr(dst) * vt->slot_bytes;
+  if (d.memMap(va, vt->slot_bytes, 0, vt->handles[size_t(src)], 0) != CUDA_SUCCESS) return ELLM_ERR_CUDA;
+  CUmemAccessDesc acc;
+  std::memset(&acc, 0, sizeof(acc));
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = vt->device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  if (d.memSetAccess(va, vt->slot_bytes, &acc, 1) != CUDA_SUCCESS) {
+    d.memUnmap(va, vt->slot_bytes);
+    return ELLM_ERR_CUDA;
+  }
+  vt->handles[size_t(dst)] = vt->handles[size_t(src)];
+  vt->mapped[size_t(dst)] = vt->owned[size_t(dst)] = 1;
+  vt->owned[size_t(src)] = 0;
+  ++vt->n_map;
+  vt->map_ns += now_ns() - t0;
+  return ELLM_OK;
+}
+
+}  // namespace ellm
+
+extern "C" {
 
 int ellm_vtensor_is_mapped(const ellm_vtensor* vt, int64_t slot) {
   if (!vt) return ELLM_ERR_INVALID_ARG;
@@ -293,7 +344,7 @@ int ellm_vtensor_destroy(ellm_vtensor* vt) {
   for (int64_t i = 0; i < vt->n_slots; ++i)
     if (vt->mapped[size_t(i)]) {
       d.memUnmap(vt->base + CUdeviceptr(i) * vt->slot_bytes, vt->slot_bytes);
-      d.memRelease(vt->handles[size_t(i)]);
+      if (vt->owned[size_t(i)]) d.memRelease(vt->handles[size_t(i)]);
     }
   if (vt->base) d.memAddressFree(vt->base, vt->slot_bytes * size_t(vt->n_slots));
   delete vt;

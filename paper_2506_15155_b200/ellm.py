@@ -42,7 +42,9 @@ class ellm_pool_config(ctypes.Structure):
 
 class ellm_stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("kv_free", "kv_used", "act", "host_free", "host_used", "n_map",
-                                               "n_unmap", "map_ns", "unmap_ns", "chunk_bytes", "mapped_bytes")]
+                                               "n_unmap", "map_ns", "unmap_ns", "chunk_bytes", "mapped_bytes",
+                                               "premapped_bytes", "pending_unmap", "crit_vmm_ns",
+                                               "n_steal", "premap_hits")]
 
 
 _P, _V = ctypes.c_void_p, ctypes.c_void_p
@@ -74,6 +76,8 @@ _SIGS = {
     "ellm_pool_grow": (ctypes.c_int, [_P, _I64]),
     "ellm_pool_shrink": (ctypes.c_int, [_P, _I64]),
     "ellm_set_swap_mode": (ctypes.c_int, [_P, _I32]),
+    "ellm_set_vmm_overlap": (ctypes.c_int, [_P, ctypes.c_int64, _I32]),
+    "ellm_vmm_sync": (ctypes.c_int, [_P]),
     "ellm_get_table": (ctypes.c_int, [_P, _I32, _P, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
     "ellm_chunk_states": (ctypes.c_int, [_P, _I64, _I64, _P]),
     "ellm_read_chunk": (ctypes.c_int, [_P, _I64, _V, _V]),
@@ -223,6 +227,13 @@ class Pool:
 
     def set_swap_mode(self, mode: int) -> int:
         return ellm_set_swap_mode(self._h, int(mode))
+
+    def set_vmm_overlap(self, premap_bytes: int = 0, async_unmap: bool = False) -> int:
+        """f1: speculative pre-mapping budget and asynchronous unmapping."""
+        return ellm_set_vmm_overlap(self._h, int(premap_bytes), int(bool(async_unmap)))
+
+    def vmm_sync(self) -> int:
+        return ellm_vmm_sync(self._h)
 
     def table(self, req):
         cap = self.cfg.max_chunks_per_request

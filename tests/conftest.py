@@ -20,6 +20,11 @@ def pytest_collection_modifyitems(config, items):
     except Exception:
         has_gpu = False
     if has_gpu:
+        # a hung kernel must fail its test, not the whole GPU session (thread method: the main
+        # thread may be blocked inside a CUDA call)
+        for it in items:
+            if "gpu" in it.keywords and it.get_closest_marker("timeout") is None:
+                it.add_marker(pytest.mark.timeout(900, method="thread"))
         return
     skip = pytest.mark.skip(reason="no CUDA device")
     for it in items:

@@ -249,13 +249,14 @@ def test_dynamic_tail_schedule(div, monkeypatch):
     tiles/div tiles of every request are claimed in units by whichever CTA is free; results
     must match the oracle exactly as the static schedule does (also fused decode)."""
     monkeypatch.setenv("ELLM_ATTN_DYN_DIV", str(div))
-    lens = [4000, 3001, 17, 2500, 1]
+    # short requests between long ones have no dynamic tiles: units span over them
+    lens = [4000, 3001, 17, 2500, 1, 40, 1800, 16, 33, 3000, 5, 2222]
     R = len(lens)
-    t = Twin(1, 32, 8, 128, 16, 800, 800, R, 260, 0, seed=13)
+    t = Twin(1, 32, 8, 128, 16, 1400, 1400, R, 260, 0, seed=13)
     reqs = list(range(R))
     assert t.reserve(reqs, lens) == 0
     t.append_all_layers(reqs, lens)
-    for _ in range(3):
+    for _ in range(6):
         t.attention(0, reqs)           # ticket counter advances across launches
     assert t.reserve(reqs, [1] * R) == 0
     assert t.decode_fused(0, reqs[::-1]) == 0
