@@ -64,6 +64,8 @@ def lib():
             "eo_release": [P, I32],
             "eo_grow": [P, I64],
             "eo_shrink": [P, I64],
+            "eo_act_alloc": [P, I64, P],
+            "eo_act_free": [P, I64],
             "eo_stats": [P, P],
             "eo_get_table": [P, I32, P, I32, P, P],
             "eo_read_chunk": [P, I64, P],
@@ -75,6 +77,8 @@ def lib():
             f = getattr(_lib, name)
             f.restype = ctypes.c_int
             f.argtypes = args
+        _lib.eo_act_used.restype = I64
+        _lib.eo_act_used.argtypes = [P]
     return _lib
 
 
@@ -110,7 +114,7 @@ def num_threads() -> int:
 
 
 class Oracle:
-    """Stateful oracle pool (SURVEY §8(c) O1-O9). Methods return (rc, outputs...)."""
+    """Stateful oracle pool (SURVEY §8(c) O1-O9, f3 O10-O11). Methods return (rc, outputs...)."""
 
     def __init__(self, n_layers, n_heads_q, n_heads_kv, head_dim, tokens_per_chunk, max_chunks,
                  initial_chunks, max_requests, max_chunks_per_request, host_slots):
@@ -181,10 +185,22 @@ class Oracle:
     def shrink(self, n):
         return lib().eo_shrink(self._h, int(n))
 
+    def act_alloc(self, n_chunks):
+        """O10 (f3): returns (rc, first chunk of the activation slot)."""
+        first = ctypes.c_int64(-1)
+        rc = lib().eo_act_alloc(self._h, int(n_chunks), ctypes.byref(first))
+        return rc, first.value
+
+    def act_free(self, first):
+        """O11 (f3)."""
+        return lib().eo_act_free(self._h, int(first))
+
     def stats(self):
         out = np.zeros(5, dtype=np.int64)
         lib().eo_stats(self._h, _ptr(out))
-        return dict(zip(("kv_free", "kv_used", "act", "host_free", "host_used"), out.tolist()))
+        d = dict(zip(("kv_free", "kv_used", "act", "host_free", "host_used"), out.tolist()))
+        d["act_used"] = int(lib().eo_act_used(self._h))
+        return d
 
     def table(self, req):
         cap = self.cfg["max_chunks_per_request"]

@@ -56,6 +56,11 @@ struct eo_state {
   int64_t row_elems = 0;     // L*2*Hkv*d (one token, all layers)
   std::vector<uint8_t> owner;     // per chunk: KV / ACT
   std::vector<uint8_t> used;      // per chunk: USED (1) / FREE (0), KV-owned only
+  // O10/O11: activation eTensor slots — runs of consecutive ACT chunks
+  // holding activations. act_len[c] = slot length if a slot starts at c, else 0;
+  // in_act[c] = chunk c belongs to a live activation slot.
+  std::vector<int64_t> act_len;
+  std::vector<uint8_t> in_act;
   std::vector<uint8_t> hused;     // per host slot
   std::map<int64_t, std::vector<uint16_t>> phys;   // chunk id -> byte image (lazy)
   std::map<int64_t, std::vector<uint16_t>> host;   // host slot -> byte image (lazy)
@@ -134,6 +139,8 @@ eo_state* eo_create(const eo_config* cfg) {
   s->chunk_elems = s->row_elems * c.tokens_per_chunk;
   // O1: ids 0..C_kv-1 are KV/FREE, the rest ACT.
   s->owner.assign(size_t(c.max_chunks), ACT);
+  s->act_len.assign(size_t(c.max_chunks), 0);
+  s->in_act.assign(size_t(c.max_chunks), 0);
   s->used.assign(size_t(c.max_chunks), 0);
   for (int64_t i = 0; i < c.initial_chunks; ++i) s->owner[size_t(i)] = KV;
   s->hused.assign(size_t(c.host_slots), 0);
@@ -384,14 +391,16 @@ int eo_release(eo_state* s, int32_t r) {
   return EO_OK;
 }
 
-// O9 — inflation (1)-(4): ownership transfer ACT -> KV and remap.
+// O9 — inflation (1)-(4): ownership transfer ACT -> KV and remap. Only chunks of
+// "inactive" activation memory can be reclaimed (step 2): chunks inside a live
+// activation slot (O10) are skipped.
 int eo_grow(eo_state* s, int64_t n) {
   if (n < 0) return EO_ERR_INVALID_ARG;
   int64_t act = 0;
-  for (uint8_t o : s->owner) act += (o == ACT);
+  for (size_t i = 0; i < s->owner.size(); ++i) act += (s->owner[i] == ACT && !s->in_act[i]);
   if (n > act) return EO_ERR_NO_CHUNKS;
   for (size_t i = 0; i < s->owner.size() && n > 0; ++i)
-    if (s->owner[i] == ACT) {
+    if (s->owner[i] == ACT && !s->in_act[i]) {
       s->owner[i] = KV;
       s->used[i] = 0;
       --n;
@@ -410,6 +419,45 @@ int eo_shrink(eo_state* s, int64_t n) {
       --n;
     }
   return EO_OK;
+}
+
+// O10 — activation eTensor allocation (f3; activation tensor slots are
+// non-uniformly sized VA segments aligned to the chunk granularity, backed by ACT-owned chunks
+// of the unified pool). A slot of n chunks is the run of n consecutive ACT chunks
+// not already in a slot whose LAST chunk has the highest id (activations fill the pool from the
+// top, KV inflation takes the lowest ACT ids). NO_CHUNKS if no such run exists.
+int eo_act_alloc(eo_state* s, int64_t n, int64_t* first_out) {
+  if (n <= 0) return EO_ERR_INVALID_ARG;
+  const int64_t C = s->c.max_chunks;
+  for (int64_t last = C - 1; last - n + 1 >= 0; --last) {
+    bool ok = true;
+    for (int64_t c = last - n + 1; c <= last && ok; ++c)
+      ok = s->owner[size_t(c)] == ACT && !s->in_act[size_t(c)];
+    if (!ok) continue;
+    const int64_t first = last - n + 1;
+    for (int64_t c = first; c <= last; ++c) s->in_act[size_t(c)] = 1;
+    s->act_len[size_t(first)] = n;
+    *first_out = first;
+    return EO_OK;
+  }
+  return EO_ERR_NO_CHUNKS;
+}
+
+// O11 — activation eTensor release: the slot starting at `first` ends; its chunks stay ACT,
+// now inactive (reclaimable by O9). Not a slot start -> NOT_MAPPED; id range -> OUT_OF_RANGE.
+int eo_act_free(eo_state* s, int64_t first) {
+  if (first < 0 || first >= s->c.max_chunks) return EO_ERR_OUT_OF_RANGE;
+  const int64_t n = s->act_len[size_t(first)];
+  if (n == 0) return EO_ERR_NOT_MAPPED;
+  for (int64_t c = first; c < first + n; ++c) s->in_act[size_t(c)] = 0;
+  s->act_len[size_t(first)] = 0;
+  return EO_OK;
+}
+
+int64_t eo_act_used(const eo_state* s) {
+  int64_t n = 0;
+  for (uint8_t a : s->in_act) n += a;
+  return n;
 }
 
 int eo_stats(const eo_state* s, int64_t* out) {
@@ -451,7 +499,7 @@ int eo_read_host_slot(const eo_state* s, int64_t h, uint8_t* dst) {
   return EO_OK;
 }
 
-// Invariants I1-I6.
+// Invariants I1-I6 and I7 (activation slots, f3).
 int eo_check_invariants(const eo_state* s) {
   const int64_t C = s->c.max_chunks, H = s->c.host_slots;
   std::vector<int> dev_refs(size_t(C), 0), host_refs(size_t(H), 0);
@@ -497,6 +545,15 @@ int eo_check_invariants(const eo_state* s) {
     if (bool(s->used[size_t(c)]) != (dev_refs[size_t(c)] == 1)) return 6;
   for (int64_t h = 0; h < H; ++h)
     if (bool(s->hused[size_t(h)]) != (host_refs[size_t(h)] == 1)) return 6;
+  // I7 (f3): activation slots are disjoint runs of ACT chunks that exactly cover in_act
+  std::vector<uint8_t> cover(size_t(C), 0);
+  for (int64_t c = 0; c < C; ++c)
+    for (int64_t k = 0; k < s->act_len[size_t(c)]; ++k) {
+      if (c + k >= C || s->owner[size_t(c + k)] != ACT || cover[size_t(c + k)]) return 7;
+      cover[size_t(c + k)] = 1;
+    }
+  for (int64_t c = 0; c < C; ++c)
+    if (cover[size_t(c)] != s->in_act[size_t(c)]) return 7;
   return 0;
 }
 

@@ -55,6 +55,14 @@ int eo_migrate(eo_state* s, int32_t n, const int32_t* src, const int32_t* dst); 
 int eo_release(eo_state* s, int32_t req);                                                      /* O8 */
 int eo_grow(eo_state* s, int64_t n);                                                           /* O9 */
 int eo_shrink(eo_state* s, int64_t n);                                                         /* O9 */
+/* f3: activation eTensor slots in the unified pool.
+ * O10 act_alloc: n consecutive ACT chunks outside any slot, the run with the highest last id;
+ *   *first_out = its first chunk. n <= 0 -> INVALID_ARG; no run -> NO_CHUNKS.
+ * O11 act_free: end the slot starting at `first` (chunks stay ACT, now reclaimable by grow).
+ * grow (O9) skips chunks inside live slots. */
+int eo_act_alloc(eo_state* s, int64_t n, int64_t* first_out);                                  /* O10 */
+int eo_act_free(eo_state* s, int64_t first);                                                   /* O11 */
+int64_t eo_act_used(const eo_state* s);   /* chunks inside live activation slots */
 /* out[5] = {kv_free, kv_used, act, host_free, host_used} */
 int eo_stats(const eo_state* s, int64_t* out);
 /* entries: >=0 device chunk id, -1 unmapped, <=-2 host slot h encoded as -(h+2) */
@@ -62,7 +70,7 @@ int eo_get_table(const eo_state* s, int32_t req, int32_t* entries, int32_t cap, 
 int eo_read_chunk(const eo_state* s, int64_t chunk, uint8_t* dst);     /* chunk_bytes; never-written bytes read 0 */
 int eo_read_host_slot(const eo_state* s, int64_t slot, uint8_t* dst);  /* chunk_bytes */
 int64_t eo_chunk_bytes(const eo_state* s);
-/* 0 if I1-I6 hold, else the number of the first violated invariant */
+/* 0 if I1-I7 hold, else the number of the first violated invariant */
 int eo_check_invariants(const eo_state* s);
 
 /* Stateless textbook attention for one request, one layer, fp64:
