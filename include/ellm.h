@@ -105,6 +105,9 @@ typedef struct {
                                       (the caller's critical path; worker time is excluded) */
   int64_t n_steal;                 /* units pool_grow backed with a pending-unmap unit's handle */
   int64_t premap_hits;             /* units pool_grow found already mapped while all-ACT */
+  /* f3 (ellm_act_*) */
+  int64_t act_used;                /* ACT chunks inside live activation slots */
+  int64_t act_cached_bytes;        /* units kept mapped only for (ended) activation slots */
 } ellm_stats;
 
 /* ---- vtensor (VMM) ------------------------------------------------------------------
@@ -234,6 +237,31 @@ int ellm_pool_shrink(ellm_pool* pool, int64_t n);
 int ellm_set_vmm_overlap(ellm_pool* pool, int64_t premap_bytes, int32_t async_unmap);
 int ellm_vmm_sync(ellm_pool* pool);
 
+/* ---- activation eTensors in the unified pool --------------
+ * act_alloc: an activation tensor slot of ceil(bytes / chunk_bytes) consecutive ACT chunks
+ *   that are not inside another slot — the run with the highest last chunk id (activations
+ *   fill the pool from the top, KV inflation takes the lowest ACT ids: DESIGN.md R15). Its
+ *   units are mapped if needed (on this thread); memory an earlier slot or KV chunk freed on
+ *   another stream is waited for on `stream`. *first_out = first chunk; *ptr_out (optional)
+ *   = device address pool_base + first*chunk_bytes (NULL on a host-only pool). bytes <= 0 ->
+ *   INVALID_ARG; no such run -> NO_CHUNKS. Chunks stay ACT-owned.
+ * act_free: end the slot starting at chunk `first` (work on `stream` so far is its last use).
+ *   Its chunks stay ACT and mapped ("mapped, available"): pool_grow can take them
+ *   as KV with no driver call (the paper's zero-overhead ownership transfer).
+ *   Not a slot start -> NOT_MAPPED; range -> OUT_OF_RANGE.
+ * act_trim: release units kept mapped only for ended slots (unmapped now, or by the f1
+ *   worker with async unmapping).
+ * pool_grow never takes chunks inside live slots (NO_CHUNKS counts only idle ACT chunks). */
+int ellm_act_alloc(ellm_pool* pool, int64_t bytes, void* stream, int64_t* first_out, void** ptr_out);
+int ellm_act_free(ellm_pool* pool, int64_t first, void* stream);
+int ellm_act_trim(ellm_pool* pool);
+/* torch.cuda.memory.CUDAPluggableAllocator hooks: allocations of a torch MemPool built on
+ * them become activation slots of the pool registered with ellm_torch_set_pool (NULL
+ * detaches). alloc returns NULL (torch raises OOM) when the pool has no fitting run. */
+int ellm_torch_set_pool(ellm_pool* pool);
+void* ellm_torch_alloc(size_t size, int device, void* stream);
+void ellm_torch_free(void* ptr, size_t size, int device, void* stream);
+
 /* Swap engine selection: 0 = SM copy kernels (default), 1 = DMA copy engines
  * (cudaMemcpyAsync per chunk). Both are exact byte copies. */
 int ellm_set_swap_mode(ellm_pool* pool, int32_t mode);
@@ -243,8 +271,9 @@ int ellm_set_swap_mode(ellm_pool* pool, int32_t mode);
 int ellm_get_table(const ellm_pool* pool, int32_t req_id, int32_t* entries, int32_t cap,
                    int32_t* n_out, int32_t* len_out);
 /* states of chunks [first, first+n): out[i] = ELLM_CHUNK_FREE (KV-owned, mapped, unused),
- * ELLM_CHUNK_USED (referenced by a table) or ELLM_CHUNK_ACT (activation-owned / unmapped). */
-enum { ELLM_CHUNK_FREE = 0, ELLM_CHUNK_USED = 1, ELLM_CHUNK_ACT = 2 };
+ * ELLM_CHUNK_USED (referenced by a table), ELLM_CHUNK_ACT (activation-owned, idle) or
+ * ELLM_CHUNK_ACT_SLOT (activation-owned, inside a live activation slot). */
+enum { ELLM_CHUNK_FREE = 0, ELLM_CHUNK_USED = 1, ELLM_CHUNK_ACT = 2, ELLM_CHUNK_ACT_SLOT = 3 };
 int ellm_chunk_states(const ellm_pool* pool, int64_t first, int64_t n, uint8_t* out);
 /* copy chunk_bytes of device chunk `chunk_id` to host_dst (synchronises `stream`). */
 int ellm_read_chunk(ellm_pool* pool, int64_t chunk_id, void* host_dst, void* stream);

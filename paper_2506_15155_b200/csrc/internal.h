@@ -241,6 +241,16 @@ struct ellm_pool {
   int64_t crit_vmm_ns = 0;           // VMM + device-sync time inside pool_grow / pool_shrink
   int64_t n_steal = 0, premap_hits = 0;
 
+  // f3: activation eTensor slots in the same pool. A slot is a run of
+  // consecutive ACT chunks; units holding live slots stay mapped, and a unit activations used
+  // stays mapped after they end ("mapped, available" pooling) until pool_grow takes
+  // its chunks (ownership transfer with no driver call) or ellm_act_trim releases it.
+  std::vector<int64_t> act_len;      // per chunk: slot length if a slot starts here, else 0
+  std::vector<uint8_t> in_act;       // per chunk: inside a live slot
+  int64_t n_act_used = 0;
+  std::vector<int32_t> unit_act;     // per unit: chunks inside live slots (under vmm_mu)
+  std::vector<uint8_t> act_cached;   // per unit: kept mapped for activations (under vmm_mu)
+
   std::map<int32_t, std::pair<CUdeviceptr, size_t>> alias;
   int last_cuda_error = 0;
   int64_t launches = 0;

@@ -192,13 +192,77 @@ int upload_ints(ellm_pool* p, const std::vector<int32_t>& v, cudaStream_t stream
 // ---- f1: VMM overlap (see ellm_pool) — the *_units helpers run with vmm_mu held -----------
 // Units that should be mapped: every unit holding a KV chunk, plus the premap window (the
 // premap_units lowest all-ACT units: pool_grow takes the lowest ACT ids next).
+inline bool unit_live(const ellm_pool* p, size_t u) {  // must stay mapped regardless of policy
+  return p->unit_kv[u] > 0 || p->unit_act[u] > 0 || p->act_cached[u];
+}
 std::vector<uint8_t> wanted_units(const ellm_pool* p) {
   std::vector<uint8_t> w(p->unit_kv.size(), 0);
   int64_t k = 0;
   for (size_t u = 0; u < w.size(); ++u)
-    if (p->unit_kv[u] > 0) w[u] = 1;
+    if (unit_live(p, u)) w[u] = 1;
     else if (k < p->premap_units) w[u] = 1, ++k;
   return w;
+}
+
+// Make every unit in `need` (sorted) mapped with its own memory, on the caller's thread (vmm_mu
+// held). A unit still mapped but "doomed" is unmapped first; with async unmapping on, a unit
+// awaiting its unmap (mapped, not live, outside the premap window, not in `keep`) donates its
+// physical handle instead of a fresh cuMemCreate (multi-mapping).
+int map_units_now(ellm_pool* p, const std::set<int64_t>& need, const std::set<int64_t>& keep) {
+  bool synced = false;
+  std::vector<int64_t> fresh;
+  for (int64_t u : need) {
+    if (p->vt->mapped[size_t(u)] && !p->doomed[size_t(u)]) continue;
+    if (p->doomed[size_t(u)]) {  // its old VA mapping must go before it is reused
+      if (!synced && cudaDeviceSynchronize() != cudaSuccess) return ELLM_ERR_CUDA;
+      synced = true;
+      if (int rc = vt_unmap_slot_nosync(p->vt, u)) return rc;
+      p->doomed[size_t(u)] = 0;
+    }
+    int64_t donor = -1;
+    if (p->async_unmap) {
+      const std::vector<uint8_t> want = wanted_units(p);
+      for (int64_t v = int64_t(p->unit_kv.size()) - 1; v >= 0 && donor < 0; --v)
+        if (p->vt->mapped[size_t(v)] && !p->doomed[size_t(v)] && !unit_live(p, size_t(v)) &&
+            !want[size_t(v)] && !keep.count(v) && !need.count(v))
+          donor = v;
+    }
+    if (donor >= 0) {
+      if (int rc = vt_map_from(p->vt, u, donor)) return rc;
+      p->doomed[size_t(donor)] = 1;
+      ++p->n_steal;
+      // the memory's pending users are those of the donor's chunks: carry their free events
+      for (int64_t k = 0; k < p->chunks_per_unit; ++k) {
+        const int64_t cu = u * p->chunks_per_unit + k, cv = donor * p->chunks_per_unit + k;
+        if (cu < p->cfg.max_chunks && cv < p->cfg.max_chunks)
+          attach_event(p, p->chunk_ev, cu, p->chunk_ev[size_t(cv)]);
+      }
+    } else {
+      fresh.push_back(u);
+    }
+  }
+  for (size_t i = 0; i < fresh.size();) {  // map contiguous runs at once
+    size_t k = i + 1;
+    while (k < fresh.size() && fresh[k] == fresh[k - 1] + 1) ++k;
+    if (int rc = ellm_vtensor_map(p->vt, fresh[i], int64_t(k - i))) return rc;
+    i = k;
+  }
+  return ELLM_OK;
+}
+
+// Synchronous release (async unmapping off): unmap the given units that are no longer wanted.
+int unmap_units_now(ellm_pool* p, std::vector<int64_t> units) {
+  const std::vector<uint8_t> want = wanted_units(p);
+  std::sort(units.begin(), units.end());
+  bool synced = false;
+  for (int64_t u : units)
+    if (!want[size_t(u)] && p->vt->mapped[size_t(u)]) {
+      if (!synced && cudaDeviceSynchronize() != cudaSuccess) return ELLM_ERR_CUDA;
+      synced = true;
+      if (int rc = vt_unmap_slot_nosync(p->vt, u)) return rc;
+      p->doomed[size_t(u)] = 0;
+    }
+  return ELLM_OK;
 }
 
 void vmm_kick(ellm_pool* p) {  // called with vmm_mu held
@@ -226,7 +290,7 @@ void vmm_worker(ellm_pool* p) {
     std::vector<uint8_t> want = wanted_units(p);
     std::vector<std::pair<int64_t, uint64_t>> cand;  // (unit, generation) before the sync
     for (size_t u = 0; u < want.size(); ++u)
-      if (p->vt->mapped[u] && p->unit_kv[u] == 0 && (p->doomed[u] || !want[u]))
+      if (p->vt->mapped[u] && !unit_live(p, u) && (p->doomed[u] || !want[u]))
         cand.push_back({int64_t(u), p->unit_gen[u]});
     if (!cand.empty()) {
       lk.unlock();
@@ -235,7 +299,7 @@ void vmm_worker(ellm_pool* p) {
       if (e != cudaSuccess) p->vmm_error = ELLM_ERR_CUDA;
       want = wanted_units(p);
       for (auto [u, gen] : cand) {  // re-check: a grow may have taken the unit back meanwhile
-        if (e != cudaSuccess || !p->vt->mapped[size_t(u)] || p->unit_kv[size_t(u)] != 0 ||
+        if (e != cudaSuccess || !p->vt->mapped[size_t(u)] || unit_live(p, size_t(u)) ||
             p->unit_gen[size_t(u)] != gen || !(p->doomed[size_t(u)] || !want[size_t(u)]))
           continue;
         if (vt_unmap_slot_nosync(p->vt, u) != ELLM_OK) p->vmm_error = ELLM_ERR_CUDA;
@@ -319,6 +383,8 @@ int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out) {
   p->slot_req.assign(size_t(c.host_slots), -1);
   p->slot_idx.assign(size_t(c.host_slots), -1);
   p->chunk_ev.assign(size_t(c.max_chunks), -1);
+  p->act_len.assign(size_t(c.max_chunks), 0);
+  p->in_act.assign(size_t(c.max_chunks), 0);
   p->slot_ev.assign(size_t(c.host_slots), -1);
   p->off_slot.assign(size_t(c.max_chunks), -1);
   p->off_layers.assign(size_t(c.max_chunks), 0);
@@ -364,6 +430,8 @@ int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out) {
   if ((rc = ellm_vtensor_create(c.device, size_t(p->unit_bytes), n_units, &p->vt))) return fail(rc);
   p->unit_kv.assign(size_t(n_units), 0);
   p->unit_gen.assign(size_t(n_units), 0);
+  p->unit_act.assign(size_t(n_units), 0);
+  p->act_cached.assign(size_t(n_units), 0);
   p->doomed.assign(size_t(n_units), 0);
   if (const char* v = std::getenv("ELLM_VMM_WORKER_DELAY_US")) p->vmm_delay_us = std::max(0L, std::atol(v));
   for (int64_t i = 0; i < c.initial_chunks; ++i) ++p->unit_kv[size_t(i / p->chunks_per_unit)];
@@ -472,11 +540,15 @@ int ellm_pool_stats(const ellm_pool* p, ellm_stats* o) {
   if (p->vt) {
     const std::vector<uint8_t> want = wanted_units(p);
     for (size_t u = 0; u < want.size(); ++u)
-      if (p->vt->mapped[u] && p->unit_kv[u] == 0) {
+      if (p->vt->mapped[u] && !unit_live(p, u)) {
         if (p->doomed[u] || !want[u]) ++o->pending_unmap;
         else o->premapped_bytes += p->unit_bytes;
       }
   }
+  o->act_used = p->n_act_used;
+  o->act_cached_bytes = 0;
+  for (size_t u = 0; u < p->act_cached.size(); ++u)
+    if (p->act_cached[u] && p->unit_act[u] == 0 && p->unit_kv[u] == 0) o->act_cached_bytes += p->unit_bytes;
   o->crit_vmm_ns = p->crit_vmm_ns;
   o->n_steal = p->n_steal;
   o->premap_hits = p->premap_hits;
@@ -1023,68 +1095,37 @@ int ellm_migrate(ellm_pool* p, int32_t n, const int32_t* src, const int32_t* dst
   return flush_table(p, S(stream));
 }
 
-// a9 — inflation (3)-(4): ACT -> KV ownership transfer + on-demand remap.
-// With f1 enabled the units it needs are usually pre-mapped already (no VMM call here); an
-// unmapped one takes the physical handle of a unit awaiting async unmap when there is one.
+// a9 — inflation (3)-(4): ACT -> KV ownership transfer + on-demand remap. Chunks
+// inside live activation slots are not reclaimable (only inactive eTensor memory).
+// Units activations used are still mapped (f3), and with f1 the next units are pre-mapped, so
+// the usual grow makes no driver call; otherwise units are mapped here (map_units_now).
 int ellm_pool_grow(ellm_pool* p, int64_t n) {
   if (!p || n < 0) return ELLM_ERR_INVALID_ARG;
-  if (n > p->n_act) return ELLM_ERR_NO_CHUNKS;
+  if (n > p->n_act - p->n_act_used) return ELLM_ERR_NO_CHUNKS;
   std::vector<int64_t> ids;
   for (int64_t c = 0; c < p->cfg.max_chunks && int64_t(ids.size()) < n; ++c)
-    if (p->owner[size_t(c)] == ACT) ids.push_back(c);
+    if (p->owner[size_t(c)] == ACT && !p->in_act[size_t(c)]) ids.push_back(c);
   std::unique_lock<std::mutex> lk(p->vmm_mu, std::defer_lock);
   if (p->has_dev) {  // map first so a driver failure leaves ownership unchanged
     lk.lock();
     const int64_t t0 = now_ns();
-    std::set<int64_t> units, need;
+    std::set<int64_t> units;
     for (int64_t c : ids) units.insert(c / p->chunks_per_unit);
     for (int64_t u : units)
-      if (!p->vt->mapped[size_t(u)] || p->doomed[size_t(u)]) need.insert(u);
-      else if (p->unit_kv[size_t(u)] == 0) ++p->premap_hits;
-    bool synced = false;
-    std::vector<int64_t> fresh;  // units mapped with new physical memory
-    for (int64_t u : need) {
-      if (p->doomed[size_t(u)]) {  // its old VA mapping must go before it is reused
-        if (!synced && cudaDeviceSynchronize() != cudaSuccess) return ELLM_ERR_CUDA;
-        synced = true;
-        if (int rc = vt_unmap_slot_nosync(p->vt, u)) return rc;
-        p->doomed[size_t(u)] = 0;
-      }
-      int64_t donor = -1;  // a mapped all-ACT unit outside the premap window: awaiting unmap
-      if (p->async_unmap) {
-        const std::vector<uint8_t> want = wanted_units(p);
-        for (int64_t v = int64_t(p->unit_kv.size()) - 1; v >= 0 && donor < 0; --v)
-          if (p->vt->mapped[size_t(v)] && !p->doomed[size_t(v)] && p->unit_kv[size_t(v)] == 0 &&
-              !want[size_t(v)] && !units.count(v))
-            donor = v;
-      }
-      if (donor >= 0) {
-        if (int rc = vt_map_from(p->vt, u, donor)) return rc;
-        p->doomed[size_t(donor)] = 1;
-        ++p->n_steal;
-        // the memory's pending users are those of the donor's chunks: carry their free events
-        for (int64_t k = 0; k < p->chunks_per_unit; ++k) {
-          const int64_t cu = u * p->chunks_per_unit + k, cv = donor * p->chunks_per_unit + k;
-          if (cu < p->cfg.max_chunks && cv < p->cfg.max_chunks)
-            attach_event(p, p->chunk_ev, cu, p->chunk_ev[size_t(cv)]);
-        }
-      } else {
-        fresh.push_back(u);
-      }
-    }
-    for (size_t i = 0; i < fresh.size();) {  // map contiguous runs at once
-      size_t k = i + 1;
-      while (k < fresh.size() && fresh[k] == fresh[k - 1] + 1) ++k;
-      if (int rc = ellm_vtensor_map(p->vt, fresh[i], int64_t(k - i))) return rc;
-      i = k;
-    }
+      if (p->vt->mapped[size_t(u)] && !p->doomed[size_t(u)] && p->unit_kv[size_t(u)] == 0) ++p->premap_hits;
+    int rc = map_units_now(p, units, units);
     p->crit_vmm_ns += now_ns() - t0;
+    if (rc) return rc;
   }
   for (int64_t c : ids) {
     p->owner[size_t(c)] = KV;
     p->used[size_t(c)] = 0;
-    if (p->has_dev && p->unit_kv[size_t(c / p->chunks_per_unit)]++ == 0)
-      ++p->unit_gen[size_t(c / p->chunks_per_unit)];
+    if (p->has_dev) {
+      const size_t u = size_t(c / p->chunks_per_unit);
+      if (!unit_live(p, u)) ++p->unit_gen[u];
+      ++p->unit_kv[u];
+      p->act_cached[u] = 0;  // the memory now belongs to the KV pool
+    }
     ++p->n_free_kv;
     --p->n_act;
     p->free_hint = std::min(p->free_hint, c);
@@ -1110,24 +1151,125 @@ int ellm_pool_shrink(ellm_pool* p, int64_t n) {
       ++p->n_act;
       --n;
       int64_t u = c / p->chunks_per_unit;
-      if (p->has_dev && --p->unit_kv[size_t(u)] == 0) units.push_back(u);
+      if (p->has_dev && --p->unit_kv[size_t(u)] == 0 && !unit_live(p, size_t(u))) units.push_back(u);
     }
   if (!p->has_dev) return ELLM_OK;
   if (!p->async_unmap && !units.empty()) {
     const int64_t t0 = now_ns();
-    const std::vector<uint8_t> want = wanted_units(p);
-    std::sort(units.begin(), units.end());
-    bool synced = false;
-    for (int64_t u : units)
-      if (!want[size_t(u)] && p->vt->mapped[size_t(u)]) {
-        if (!synced && cudaDeviceSynchronize() != cudaSuccess) return ELLM_ERR_CUDA;
-        synced = true;
-        if (int rc = vt_unmap_slot_nosync(p->vt, u)) return rc;
-      }
+    int rc = unmap_units_now(p, units);
     p->crit_vmm_ns += now_ns() - t0;
+    if (rc) return rc;
   }
   vmm_kick(p);
   return ELLM_OK;
+}
+
+// ---- f3: activation eTensors in the unified pool ------------------------------
+// O10: a slot of ceil(bytes / chunk_bytes) consecutive idle ACT chunks, the run with the highest
+// last id (activations fill the pool from the top; KV inflation takes the lowest ids).
+int ellm_act_alloc(ellm_pool* p, int64_t bytes, void* stream, int64_t* first_out, void** ptr_out) {
+  if (!p || bytes <= 0 || !first_out) return ELLM_ERR_INVALID_ARG;
+  const int64_t n = (bytes + p->chunk_bytes - 1) / p->chunk_bytes;
+  int64_t first = -1, run = 0;
+  for (int64_t c = p->cfg.max_chunks - 1; c >= 0; --c) {
+    run = (p->owner[size_t(c)] == ACT && !p->in_act[size_t(c)]) ? run + 1 : 0;
+    if (run == n) {
+      first = c;
+      break;
+    }
+  }
+  if (first < 0) return ELLM_ERR_NO_CHUNKS;
+  if (p->has_dev) {
+    std::lock_guard<std::mutex> g(p->vmm_mu);
+    const int64_t t0 = now_ns();
+    std::set<int64_t> units;
+    for (int64_t c = first; c < first + n; ++c) units.insert(c / p->chunks_per_unit);
+    int rc = map_units_now(p, units, units);
+    p->crit_vmm_ns += now_ns() - t0;
+    if (rc) return rc;
+    for (int64_t c = first; c < first + n; ++c) {
+      const size_t u = size_t(c / p->chunks_per_unit);
+      if (!unit_live(p, u)) ++p->unit_gen[u];
+      ++p->unit_act[u];
+      p->act_cached[u] = 1;
+      cudaError_t e = wait_freed(p, p->chunk_ev, c, S(stream));  // memory freed on another stream
+      if (e != cudaSuccess) return cuda_fail(p, e);
+    }
+    vmm_kick(p);
+  }
+  for (int64_t c = first; c < first + n; ++c) p->in_act[size_t(c)] = 1;
+  p->act_len[size_t(first)] = n;
+  p->n_act_used += n;
+  *first_out = first;
+  if (ptr_out) *ptr_out = p->has_dev ? static_cast<uint8_t*>(ellm_vtensor_base(p->vt)) + first * p->chunk_bytes : nullptr;
+  return ELLM_OK;
+}
+
+// O11: the slot starting at `first` ends; its chunks stay ACT and mapped (reclaimable by grow).
+// Work on `stream` so far is the slot's last use (stream-ordered reuse, as for KV chunks).
+int ellm_act_free(ellm_pool* p, int64_t first, void* stream) {
+  if (!p) return ELLM_ERR_INVALID_ARG;
+  if (first < 0 || first >= p->cfg.max_chunks) return ELLM_ERR_OUT_OF_RANGE;
+  const int64_t n = p->act_len[size_t(first)];
+  if (n == 0) return ELLM_ERR_NOT_MAPPED;
+  if (p->has_dev) {
+    std::lock_guard<std::mutex> g(p->vmm_mu);
+    const int32_t ev = record_free_event(p, S(stream));
+    if (ev < 0) return cuda_fail(p, cudaGetLastError());
+    for (int64_t c = first; c < first + n; ++c) {
+      attach_event(p, p->chunk_ev, c, ev);
+      --p->unit_act[size_t(c / p->chunks_per_unit)];
+    }
+    if (p->free_events[size_t(ev)].refs == 0) p->free_event_pool.push_back(ev);
+  }
+  for (int64_t c = first; c < first + n; ++c) p->in_act[size_t(c)] = 0;
+  p->act_len[size_t(first)] = 0;
+  p->n_act_used -= n;
+  return ELLM_OK;
+}
+
+// Release the activation cache: units kept mapped only because activations used them.
+int ellm_act_trim(ellm_pool* p) {
+  if (!p) return ELLM_ERR_INVALID_ARG;
+  if (!p->has_dev) return ELLM_OK;
+  std::lock_guard<std::mutex> g(p->vmm_mu);
+  std::vector<int64_t> units;
+  for (size_t u = 0; u < p->act_cached.size(); ++u)
+    if (p->act_cached[u] && p->unit_act[u] == 0) {
+      p->act_cached[u] = 0;
+      if (p->unit_kv[u] == 0) units.push_back(int64_t(u));
+    }
+  if (!p->async_unmap && !units.empty()) {
+    const int64_t t0 = now_ns();
+    int rc = unmap_units_now(p, units);
+    p->crit_vmm_ns += now_ns() - t0;
+    if (rc) return rc;
+  }
+  vmm_kick(p);
+  return ELLM_OK;
+}
+
+// torch.cuda.memory.CUDAPluggableAllocator entry points (the framework's caching
+// allocator keeps its BFC strategy on top; its segments come from activation slots).
+static ellm_pool* g_torch_pool = nullptr;
+int ellm_torch_set_pool(ellm_pool* p) {
+  g_torch_pool = p;
+  return ELLM_OK;
+}
+void* ellm_torch_alloc(size_t size, int device, void* stream) {
+  ellm_pool* p = g_torch_pool;
+  if (!p || !p->has_dev || device != p->cfg.device || size == 0) return nullptr;
+  int64_t first = -1;
+  void* ptr = nullptr;
+  return ellm_act_alloc(p, int64_t(size), stream, &first, &ptr) == ELLM_OK ? ptr : nullptr;
+}
+void ellm_torch_free(void* ptr, size_t size, int device, void* stream) {
+  (void)size;
+  (void)device;
+  ellm_pool* p = g_torch_pool;
+  if (!p || !p->has_dev || !ptr) return;
+  const int64_t off = static_cast<uint8_t*>(ptr) - static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
+  if (off >= 0 && off % p->chunk_bytes == 0) ellm_act_free(p, off / p->chunk_bytes, stream);
 }
 
 int ellm_set_vmm_overlap(ellm_pool* p, int64_t premap_bytes, int32_t async_unmap) {
@@ -1170,7 +1312,8 @@ int ellm_chunk_states(const ellm_pool* p, int64_t first, int64_t n, uint8_t* out
   if (first < 0 || first + n > p->cfg.max_chunks) return ELLM_ERR_OUT_OF_RANGE;
   for (int64_t i = 0; i < n; ++i) {
     const size_t c = size_t(first + i);
-    out[i] = p->owner[c] == ACT ? ELLM_CHUNK_ACT : p->used[c] ? ELLM_CHUNK_USED : ELLM_CHUNK_FREE;
+    out[i] = p->owner[c] == ACT ? (p->in_act[c] ? ELLM_CHUNK_ACT_SLOT : ELLM_CHUNK_ACT)
+                                : p->used[c] ? ELLM_CHUNK_USED : ELLM_CHUNK_FREE;
   }
   return ELLM_OK;
 }

@@ -44,7 +44,7 @@ class ellm_stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("kv_free", "kv_used", "act", "host_free", "host_used", "n_map",
                                                "n_unmap", "map_ns", "unmap_ns", "chunk_bytes", "mapped_bytes",
                                                "premapped_bytes", "pending_unmap", "crit_vmm_ns",
-                                               "n_steal", "premap_hits")]
+                                               "n_steal", "premap_hits", "act_used", "act_cached_bytes")]
 
 
 _P, _V = ctypes.c_void_p, ctypes.c_void_p
@@ -78,6 +78,12 @@ _SIGS = {
     "ellm_set_swap_mode": (ctypes.c_int, [_P, _I32]),
     "ellm_set_vmm_overlap": (ctypes.c_int, [_P, ctypes.c_int64, _I32]),
     "ellm_vmm_sync": (ctypes.c_int, [_P]),
+    "ellm_act_alloc": (ctypes.c_int, [_P, ctypes.c_int64, _P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_P)]),
+    "ellm_act_free": (ctypes.c_int, [_P, ctypes.c_int64, _P]),
+    "ellm_act_trim": (ctypes.c_int, [_P]),
+    "ellm_torch_set_pool": (ctypes.c_int, [_P]),
+    "ellm_torch_alloc": (_P, [ctypes.c_size_t, ctypes.c_int, _P]),
+    "ellm_torch_free": (None, [_P, ctypes.c_size_t, ctypes.c_int, _P]),
     "ellm_get_table": (ctypes.c_int, [_P, _I32, _P, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
     "ellm_chunk_states": (ctypes.c_int, [_P, _I64, _I64, _P]),
     "ellm_read_chunk": (ctypes.c_int, [_P, _I64, _V, _V]),
@@ -235,6 +241,31 @@ class Pool:
     def vmm_sync(self) -> int:
         return ellm_vmm_sync(self._h)
 
+    # ---- f3: activation eTensors in the unified pool ----
+    def act_alloc(self, nbytes_or_chunks, stream=None, chunks=True):
+        """Activation slot; returns (rc, first chunk). `chunks=True`: the size is in chunks."""
+        nbytes = int(nbytes_or_chunks) * self.chunk_bytes if chunks else int(nbytes_or_chunks)
+        first = ctypes.c_int64(-1)
+        ptr = _P()
+        rc = ellm_act_alloc(self._h, nbytes, _sptr(stream), ctypes.byref(first), ctypes.byref(ptr))
+        self._last_act_ptr = ptr.value
+        return rc, first.value
+
+    def act_free(self, first, stream=None) -> int:
+        return ellm_act_free(self._h, int(first), _sptr(stream))
+
+    def act_trim(self) -> int:
+        return ellm_act_trim(self._h)
+
+    def activation_mempool(self):
+        """A torch.cuda.MemPool whose segments are activation slots of this pool (torch's
+        caching allocator keeps its best-fit/coalescing strategy on top). Use with
+        torch.cuda.use_mem_pool(mp). One pool at a time is registered for the hooks."""
+        import torch
+        ellm_torch_set_pool(self._h)
+        alloc = torch.cuda.memory.CUDAPluggableAllocator(LIB_PATH, "ellm_torch_alloc", "ellm_torch_free")
+        return torch.cuda.MemPool(alloc.allocator())
+
     def table(self, req):
         cap = self.cfg.max_chunks_per_request
         ent = np.full(cap, -1, np.int32)
@@ -245,7 +276,7 @@ class Pool:
         return ent[: n.value].copy(), ln.value
 
     def chunk_states(self) -> np.ndarray:
-        """uint8 [max_chunks]: 0 FREE, 1 USED, 2 ACT."""
+        """uint8 [max_chunks]: 0 FREE, 1 USED, 2 ACT (idle), 3 ACT inside a live activation slot."""
         out = np.zeros(self.cfg.max_chunks, np.uint8)
         rc = ellm_chunk_states(self._h, 0, self.cfg.max_chunks, _ptr(out))
         if rc != OK:

@@ -44,7 +44,7 @@ def test_c1_tables_closed_form():
     assert o.reserve([0, 1, 2, 3], [1, 1, 1, 1]) == oracle.OK
     for r, want in enumerate(g["tables_after_one_decode"]):
         assert o.table(r)[0].tolist() == want
-    assert o.stats() == g["stats_after_one_decode"]
+    assert o.stats() == {**g["stats_after_one_decode"], "act_used": 0}
     assert o.check_invariants() == 0
 
 
@@ -118,7 +118,7 @@ def test_migrate_compaction_closed_form():
     assert t3[-4:] == [5, 4, 3, 2]
     assert o.stats()["kv_used"] == 30
     assert o.shrink(34) == oracle.OK          # ids 30..63 are FREE now: exactly 34
-    assert o.stats() == {"kv_free": 0, "kv_used": 30, "act": 34, "host_free": 64, "host_used": 0}
+    assert o.stats() == {"kv_free": 0, "kv_used": 30, "act": 34, "host_free": 64, "host_used": 0, "act_used": 0}
     assert o.shrink(1) == oracle.IN_USE
     assert o.grow(2) == oracle.OK             # lowest ACT ids: 30, 31
     assert o.reserve([1], [20]) == oracle.OK

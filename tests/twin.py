@@ -153,6 +153,16 @@ class Twin:
         assert a == b
         return a
 
+    def act_alloc(self, n_chunks):
+        a, b = self.o.act_alloc(n_chunks), self.p.act_alloc(n_chunks)
+        assert a[0] == b[0] and (a[0] != 0 or a[1] == b[1]), (a, b)
+        return a
+
+    def act_free(self, first):
+        a, b = self.o.act_free(first), self.p.act_free(first)
+        assert a == b, (a, b)
+        return a
+
     # ---- state checks ---------------------------------------------------------------
     def check_tables(self):
         for r in range(self.R):
