@@ -1,7 +1,7 @@
 """Pins for the oracle's activation eTensor slots (O10/O11 in oracle.h) and
 for grow's skipping of live slots (O9; "unmaps physical memory chunks allocated to
 inactive eTensor objects"). Every expected value below is derived by hand from the written
-policy (R15): a slot is the run of consecutive idle ACT chunks with the highest last
+policy (R15/R16): a slot is the run of consecutive idle ACT chunks with the highest last
 id; grow takes the lowest idle ACT ids. A product-side twin on a host-only pool (no GPU) must
 reach the same states.
 """
