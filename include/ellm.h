@@ -240,7 +240,7 @@ int ellm_vmm_sync(ellm_pool* pool);
 /* ---- activation eTensors in the unified pool --------------
  * act_alloc: an activation tensor slot of ceil(bytes / chunk_bytes) consecutive ACT chunks
  *   that are not inside another slot — the run with the highest last chunk id (activations
- *   fill the pool from the top, KV inflation takes the lowest ACT ids: DESIGN.md R15). Its
+ *   fill the pool from the top, KV inflation takes the lowest ACT ids: DESIGN.md R16). Its
  *   units are mapped if needed (on this thread); memory an earlier slot or KV chunk freed on
  *   another stream is waited for on `stream`. *first_out = first chunk; *ptr_out (optional)
  *   = device address pool_base + first*chunk_bytes (NULL on a host-only pool). bytes <= 0 ->
