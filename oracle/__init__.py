@@ -58,6 +58,7 @@ def lib():
             "eo_reserve": [P, I32, P, P],
             "eo_append": [P, I32, I32, P, P, P, P],
             "eo_attention": [P, I32, I32, P, P, ctypes.c_double, P, I32],
+            "eo_prefill_attention": [P, I32, I32, P, P, P, ctypes.c_double, P, I32],
             "eo_deflate": [P, I32, P, P],
             "eo_inflate": [P, I32, P, P],
             "eo_migrate": [P, I32, P, P],
@@ -156,6 +157,16 @@ class Oracle:
         out = np.zeros((len(r), self.cfg["n_heads_q"], self.cfg["head_dim"]), dtype=np.float64)
         rc = lib().eo_attention(self._h, layer, len(r), _ptr(r), _ptr(q), float(scale), _ptr(out),
                                 1 if through_table else 0)
+        return rc, out
+
+    def prefill_attention(self, layer, reqs, n_q, q_bits, scale, through_table=True):
+        """O12 (f4): causal attention of the last n_q[i] positions of each request."""
+        r, nq = _i32(reqs), _i32(n_q)
+        q = np.ascontiguousarray(q_bits, dtype=np.uint16)
+        rows = int(nq.sum()) if len(nq) else 0
+        out = np.zeros((rows, self.cfg["n_heads_q"], self.cfg["head_dim"]), dtype=np.float64)
+        rc = lib().eo_prefill_attention(self._h, layer, len(r), _ptr(r), _ptr(nq), _ptr(q), float(scale),
+                                        _ptr(out), 1 if through_table else 0)
         return rc, out
 
     def deflate(self, ids):

@@ -35,3 +35,26 @@ def attention(q_bits: np.ndarray, k_bits: np.ndarray, v_bits: np.ndarray, scale:
     w = np.exp(s)
     w = w / w.sum(axis=1, keepdims=True)
     return np.einsum("hj,jhd->hd", w, v_full)
+
+
+def causal_prefill(q_bits: np.ndarray, k_bits: np.ndarray, v_bits: np.ndarray, scale: float) -> np.ndarray:
+    """Causal attention of the LAST nq positions of a sequence (f4).
+
+    q_bits [nq, Hq, d]; k_bits/v_bits [len, Hkv, d]. Query i sits at position len - nq + i and
+    sees keys 0..that position: a lower-triangular mask on the [nq, len] score matrix.
+    Returns [nq, Hq, d] float64."""
+    q = bf16_bits_to_f64(q_bits)
+    k = bf16_bits_to_f64(k_bits)
+    v = bf16_bits_to_f64(v_bits)
+    nq, Hq, _ = q.shape
+    n = k.shape[0]
+    group = Hq // k.shape[1]
+    k_full = np.repeat(k, group, axis=1)                      # [len, Hq, d]
+    v_full = np.repeat(v, group, axis=1)
+    s = scale * np.einsum("ihd,jhd->hij", q, k_full)            # [Hq, nq, len]
+    pos = np.arange(nq)[:, None] + (n - nq)
+    s = np.where(np.arange(n)[None, :] <= pos, s, -np.inf)
+    s = s - s.max(axis=2, keepdims=True)
+    w = np.exp(s)
+    w = w / w.sum(axis=2, keepdims=True)
+    return np.einsum("hij,jhd->ihd", w, v_full)

@@ -300,6 +300,54 @@ int eo_attention(eo_state* s, int32_t layer, int32_t n, const int32_t* reqs, con
   return EO_OK;
 }
 
+// O12 (P:871 chunked prefill over the KV cache) — causal attention of the
+// last n_q[i] positions of each listed request: query k (q row cum + k) sits at position
+// P = len - n_q + k and attends keys 0..P (each token attends to the tokens before
+// it and itself). Written as that definition: the decode routine applied to the first P+1
+// keys, read through the page table (or from the contiguous copy with through_table = 0).
+int eo_prefill_attention(eo_state* s, int32_t layer, int32_t n, const int32_t* reqs,
+                         const int32_t* n_q, const uint16_t* q, double scale, double* out,
+                         int32_t through_table) {
+  if (layer < 0 || layer >= s->c.n_layers) return EO_ERR_OUT_OF_RANGE;
+  if (n < 0) return EO_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (reqs[i] < 0 || reqs[i] >= s->c.max_requests) return EO_ERR_OUT_OF_RANGE;
+  for (int32_t i = 0; i < n; ++i) {
+    const int64_t len = s->req[size_t(reqs[i])].len;
+    if (len == 0 || n_q[i] < 1 || n_q[i] > len) return EO_ERR_INVALID_ARG;
+  }
+  for (int32_t i = 0; i < n; ++i) {
+    const Request& R = s->req[size_t(reqs[i])];
+    for (int64_t ci = 0; ci < s->nchunks_of(R.len); ++ci)
+      if (!is_dev(R.pt[size_t(ci)])) return EO_ERR_NOT_RESIDENT;
+  }
+  const int64_t Hq = s->c.n_heads_q, Hkv = s->c.n_heads_kv, d = s->c.head_dim;
+  int64_t row = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    Request& R = s->req[size_t(reqs[i])];
+    std::vector<uint16_t> k(size_t(R.len * Hkv * d)), v(size_t(R.len * Hkv * d));
+    for (int64_t p = 0; p < R.len; ++p)
+      for (int64_t h = 0; h < Hkv; ++h)
+        for (int64_t e = 0; e < d; ++e) {
+          size_t o = size_t((p * Hkv + h) * d + e);
+          if (through_table) {
+            const std::vector<uint16_t>& img = s->phys_img(R.pt[size_t(p / s->T())]);
+            k[o] = img[size_t(s->chunk_off(layer, 0, h, p % s->T()) + e)];
+            v[o] = img[size_t(s->chunk_off(layer, 1, h, p % s->T()) + e)];
+          } else {
+            k[o] = R.kv[size_t(s->contig_off(p, layer, 0, h) + e)];
+            v[o] = R.kv[size_t(s->contig_off(p, layer, 1, h) + e)];
+          }
+        }
+    for (int64_t kq = 0; kq < n_q[i]; ++kq, ++row) {
+      const int64_t P = R.len - n_q[i] + kq;  // keys 0..P (K/V are token-major: a prefix)
+      eo_attention_contig(int32_t(Hq), int32_t(Hkv), int32_t(d), int32_t(P + 1), q + row * Hq * d,
+                          k.data(), v.data(), scale, out + row * Hq * d);
+    }
+  }
+  return EO_OK;
+}
+
 // O5 — offload KV chunks to CPU DRAM; deflation is the reverse of
 // inflation. Lowest free host slot first, in list order (DESIGN R7).
 int eo_deflate(eo_state* s, int32_t n, const int32_t* ids, int32_t* slots_out) {

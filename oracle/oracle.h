@@ -49,6 +49,13 @@ int eo_append(eo_state* s, int32_t layer, int32_t n, const int32_t* reqs, const 
               const uint16_t* k_new, const uint16_t* v_new);                                   /* O3 */
 int eo_attention(eo_state* s, int32_t layer, int32_t n, const int32_t* reqs, const uint16_t* q,
                  double scale, double* out, int32_t through_table);                            /* O4 */
+/* O12 (f4): causal attention of the last n_q[i] positions of each listed request (n_q in
+ * [1, len], else INVALID_ARG). q [sum n_q][Hq][d] bf16 bits, rows in list order then position
+ * order; out [sum n_q][Hq][d] fp64. Query k of request i (position P = len - n_q + k) attends
+ * keys 0..P. Residency / range errors as eo_attention. */
+int eo_prefill_attention(eo_state* s, int32_t layer, int32_t n, const int32_t* reqs,
+                         const int32_t* n_q, const uint16_t* q, double scale, double* out,
+                         int32_t through_table);                                              /* O12 */
 int eo_deflate(eo_state* s, int32_t n, const int32_t* ids, int32_t* slots_out);               /* O5 */
 int eo_inflate(eo_state* s, int32_t n, const int32_t* slots, int32_t* ids_out);               /* O6 */
 int eo_migrate(eo_state* s, int32_t n, const int32_t* src, const int32_t* dst);               /* O7 */
