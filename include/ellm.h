@@ -172,6 +172,19 @@ int ellm_decode_append_attention(ellm_pool* pool, int32_t layer, int32_t n, cons
                                  const void* k_new, const void* v_new, const void* q, void* out,
                                  float softmax_scale, void* stream);
 
+/* prefill_attention (P:871 chunked prefill, P:109-112 causal attention):
+ * for each listed request i, the LAST n_q[i] positions (the chunk just reserved and appended)
+ * attend causally to the request's KV read through its chunk table: query k of request i sits
+ * at position P = len - n_q[i] + k and out row = sum_{j <= P} softmax_j(scale * q.k_j) v_j per
+ * q-head (kv-head h / (Hq/Hkv)). q: device [sum n_q, Hq, d] bf16, rows in list order then
+ * position order; out: device [sum n_q, Hq, d] bf16 (fp32 accumulate, RNE). Runs on the
+ * tcgen05 tensor cores (S and O in tensor memory). Errors: layer / id range -> OUT_OF_RANGE;
+ * n_q[i] < 1 or > len -> INVALID_ARG; a chunk in a host slot -> NOT_RESIDENT; Hq/Hkv not
+ * dividing 128 or more than 32768 work items (request x kv-head x 128/group positions) ->
+ * UNSUPPORTED. */
+int ellm_prefill_attention(ellm_pool* pool, int32_t layer, int32_t n, const int32_t* req_ids,
+                           const int32_t* n_q, const void* q, void* out, float softmax_scale, void* stream);
+
 /* release: all device chunks and host slots of req become FREE; len = 0. */
 int ellm_release(ellm_pool* pool, int32_t req_id, void* stream);
 

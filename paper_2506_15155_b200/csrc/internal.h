@@ -143,6 +143,15 @@ cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh,
                                    const void* q, void* out, float* part, float* part_ml,
                                    int32_t* arrivals, float scale, cudaStream_t s, int* launches);
 
+// chunked-prefill attention (prefill.cu). work: [n_work][8] int32 items
+// {req, len, q_row0, p0, n_valid, kvh, n_tiles, 0}.
+cudaError_t encode_prefill_maps(CUtensorMap* kvmap, CUtensorMap* qmap, void* pool_base, int64_t max_chunks,
+                                const AttnShape& sh, const void* q, int64_t q_rows);
+cudaError_t launch_prefill_attention(const CUtensorMap& kvmap, const CUtensorMap& qmap, const AttnShape& sh,
+                                     const int32_t* work, int32_t n_work, const int32_t* table,
+                                     int32_t table_stride, int32_t layer, void* out, float scale,
+                                     cudaStream_t s);
+
 }  // namespace ellm
 
 // ---- the pool ---------------------------------------------------------------------------

@@ -1272,6 +1272,59 @@ void ellm_torch_free(void* ptr, size_t size, int device, void* stream) {
   if (off >= 0 && off % p->chunk_bytes == 0) ellm_act_free(p, off / p->chunk_bytes, stream);
 }
 
+// ---- f4: chunked-prefill attention (prefill.cu) ------------------------------------
+// Work items: (request, kv-head, block of 128/group query positions), longest first.
+int ellm_prefill_attention(ellm_pool* p, int32_t layer, int32_t n, const int32_t* reqs, const int32_t* n_q,
+                           const void* q, void* out, float scale, void* stream) {
+  if (!p) return ELLM_ERR_INVALID_ARG;
+  if (!p->has_dev) return ELLM_ERR_NO_DEVICE;
+  if (layer < 0 || layer >= p->cfg.n_layers) return ELLM_ERR_OUT_OF_RANGE;
+  if (n < 0 || (n > 0 && (!reqs || !n_q || !q || !out))) return ELLM_ERR_INVALID_ARG;
+  if (!check_reqs_range(p, n, reqs)) return ELLM_ERR_OUT_OF_RANGE;
+  if (128 % p->group != 0) return ELLM_ERR_UNSUPPORTED;
+  int64_t rows = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    const int64_t len = p->len[size_t(reqs[i])];
+    if (len == 0 || n_q[i] < 1 || n_q[i] > len) return ELLM_ERR_INVALID_ARG;
+    rows += n_q[i];
+  }
+  for (int32_t i = 0; i < n; ++i)
+    if (p->nonres[size_t(reqs[i])] > 0) return ELLM_ERR_NOT_RESIDENT;
+  if (n == 0) return ELLM_OK;
+  cudaStream_t st = S(stream);
+  if (int rc = flush_table(p, st)) return rc;
+  const int bp = 128 / p->group;  // query positions per block
+  struct Item { int32_t v[8]; };
+  std::vector<Item> items;
+  int64_t row0 = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t r = reqs[i];
+    const int64_t len = p->len[size_t(r)];
+    for (int64_t b = 0; b < n_q[i]; b += bp) {
+      const int64_t pos0 = len - n_q[i] + b;
+      const int64_t nv = std::min<int64_t>(bp, n_q[i] - b);
+      const int64_t tiles = (pos0 + nv + 127) / 128;  // keys 0 .. pos0 + nv - 1
+      for (int32_t h = 0; h < p->cfg.n_heads_kv; ++h)
+        items.push_back({{r, int32_t(len), int32_t(row0 + b), int32_t(pos0), int32_t(nv), h, int32_t(tiles), 0}});
+    }
+    row0 += n_q[i];
+  }
+  std::stable_sort(items.begin(), items.end(), [](const Item& a, const Item& b) { return a.v[6] > b.v[6]; });
+  std::vector<int32_t> flat(items.size() * 8);
+  for (size_t i = 0; i < items.size(); ++i) std::memcpy(&flat[i * 8], items[i].v, 32);
+  const int32_t* d_work = nullptr;
+  if (flat.size() * 4 > p->ring.seg_bytes()) return ELLM_ERR_UNSUPPORTED;  // > 32K work items
+  if (int rc = upload_ints(p, flat, st, &d_work, nullptr)) return rc;
+  CUtensorMap kvmap, qmap;
+  cudaError_t e = encode_prefill_maps(&kvmap, &qmap, ellm_vtensor_base(p->vt), p->cfg.max_chunks, p->ash, q, rows);
+  if (e != cudaSuccess) return cuda_fail(p, e);
+  e = launch_prefill_attention(kvmap, qmap, p->ash, d_work, int32_t(items.size()), p->d_table,
+                               p->cfg.max_chunks_per_request, layer, out, scale, st);
+  if (e != cudaSuccess) return cuda_fail(p, e);
+  ++p->launches;
+  return p->ring.commit(st);
+}
+
 int ellm_set_vmm_overlap(ellm_pool* p, int64_t premap_bytes, int32_t async_unmap) {
   if (!p || premap_bytes < 0 || (async_unmap != 0 && async_unmap != 1)) return ELLM_ERR_INVALID_ARG;
   if (!p->has_dev) return ELLM_ERR_NO_DEVICE;

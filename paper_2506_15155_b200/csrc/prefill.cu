@@ -1,0 +1,442 @@
+// prefill.cu — chunked-prefill attention over chunk-mapped KV on the 5th-generation tensor cores
+// ("chunked prefill"; P:109-112 causal attention over the KV cache).
+//
+// Computes, for the last n_q positions of each listed request (query k at position
+// P = len - n_q + k) and every q-head h (kv-head g = h / group, R6):
+//     o = sum_{j <= P} softmax_j(scale * q.k_j) v_j,
+// reading k_j, v_j through the request's chunk table (R3).
+//
+// B200 design (f4):
+//  * One CTA per work item = (request, kv-head, block of 128/group query positions). Its M = 128
+//    MMA rows are (position, q-head of the group) pairs, so one K/V tile feeds every head of the
+//    group. Items are ordered by decreasing tile count (longest first).
+//  * Warp 0: TMA producer. Q once (SWIZZLE_128B, K-major rows), then per 128-key tile the
+//    chunk table's pieces: one TMA box (64 d-elements x min(T,128) tokens) per (piece, K/V,
+//    64-wide half of d) into a 2-stage mbarrier ring laid out [half][token][64] — the canonical
+//    UMMA K-major layout for K and MN-major layout for V.
+//  * Warp 1: allocates 512 TMEM columns and issues tcgen05.mma (one thread): S = Q.K^T into a
+//    double-buffered fp32 TMEM tile (cols 0-127 / 128-255), then O += P.V into cols 256+
+//    (P from shared memory, V MN-major), committing to mbarriers (tcgen05.commit).
+//  * Warps 2-5: softmax, one thread per TMEM lane = one MMA row. tcgen05.ld of the S row, causal
+//    mask, base-2 online softmax with lazy rescaling (O in TMEM is rescaled only when the row max
+//    grows by more than 2^8), P written as bf16 into shared memory in the swizzled K-major layout,
+//    and at the end O / l -> bf16 -> global.
+#include <cuda_bf16.h>
+
+#include "internal.h"
+
+namespace ellm {
+namespace {
+
+constexpr int kM = 128;         // MMA rows per CTA
+constexpr int kN = 128;         // keys per tile
+constexpr int kStages = 2;      // K/V ring depth
+constexpr int kThreads = 192;   // warp 0 TMA, warp 1 MMA, warps 2..5 softmax
+constexpr uint32_t kTmemCols = 512;
+constexpr float kRescaleHeadroom = 8.f;  // log2 units: P <= 2^8 before O is rescaled
+
+template <int D>
+struct Layout {
+  static constexpr int TILE = kN * D * 2;  // one K or V tile: [D/64][128 tokens][64] bf16
+  static constexpr int Q = kM * D * 2;     // [D/64][128 rows][64]
+  static constexpr int P = kM * kN * 2;    // [2 token halves][128 rows][64]
+  static constexpr int off_q = 0;
+  static constexpr int off_kv = Q;         // stage s: K at off_kv + 2*s*TILE, V at + TILE
+  static constexpr int off_p = off_kv + kStages * 2 * TILE;
+  static constexpr int off_bar = off_p + P;
+  // >= 116 KB so one CTA owns an SM (its 512 TMEM columns are the whole TMEM)
+  static constexpr int bytes = (off_bar + 256 + 1024) > 118784 ? (off_bar + 256 + 1024) : 118784;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                       uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_5d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                       int c4, uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar),
+      "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// ---- tcgen05 -------------------------------------------------------------------------------
+// Shared-memory matrix descriptor (sm100 "version 1"), 128-byte swizzle, 8-row atoms of
+// 1024 B. K-major: rows of 64 elements, LBO unused (16 B), SBO = 1024 B between 8-row groups.
+// MN-major: 64-element MN blocks `lbo` bytes apart, 8-row K groups 1024 B apart.
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo) {
+  return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
+         (uint64_t(1024 >> 4) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+// Instruction descriptor, kind::f16: fp32 accumulate, bf16 A and B, A K-major, B K- or MN-major.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool b_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(b_mn_major) << 16) | (uint32_t(N >> 3) << 17) |
+         (uint32_t(M >> 4) << 24);
+}
+__device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+#define ELLM_R32(i) "=r"(r[i])
+// 32 consecutive TMEM columns of this thread's lane -> registers
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : ELLM_R32(0), ELLM_R32(1), ELLM_R32(2), ELLM_R32(3), ELLM_R32(4), ELLM_R32(5), ELLM_R32(6), ELLM_R32(7),
+        ELLM_R32(8), ELLM_R32(9), ELLM_R32(10), ELLM_R32(11), ELLM_R32(12), ELLM_R32(13), ELLM_R32(14),
+        ELLM_R32(15), ELLM_R32(16), ELLM_R32(17), ELLM_R32(18), ELLM_R32(19), ELLM_R32(20), ELLM_R32(21),
+        ELLM_R32(22), ELLM_R32(23), ELLM_R32(24), ELLM_R32(25), ELLM_R32(26), ELLM_R32(27), ELLM_R32(28),
+        ELLM_R32(29), ELLM_R32(30), ELLM_R32(31)
+      : "r"(taddr));
+}
+#undef ELLM_R32
+#define ELLM_W32(i) "r"(r[i])
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      ELLM_W32(0), ELLM_W32(1), ELLM_W32(2), ELLM_W32(3), ELLM_W32(4), ELLM_W32(5), ELLM_W32(6), ELLM_W32(7),
+      ELLM_W32(8), ELLM_W32(9), ELLM_W32(10), ELLM_W32(11), ELLM_W32(12), ELLM_W32(13), ELLM_W32(14), ELLM_W32(15),
+      ELLM_W32(16), ELLM_W32(17), ELLM_W32(18), ELLM_W32(19), ELLM_W32(20), ELLM_W32(21), ELLM_W32(22),
+      ELLM_W32(23), ELLM_W32(24), ELLM_W32(25), ELLM_W32(26), ELLM_W32(27), ELLM_W32(28), ELLM_W32(29),
+      ELLM_W32(30), ELLM_W32(31)
+      : "memory");
+}
+#undef ELLM_W32
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+struct PParams {
+  const int4* work;        // [n_work][2]: {req, len, q_row0, p0}, {n_valid, kvh, n_tiles, 0}
+  const int32_t* table;
+  __nv_bfloat16* out;      // [rows][Hq][D]
+  int32_t table_stride, Hq, group, T, L, layer;
+  float scale_log2;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    prefill_kernel(const __grid_constant__ CUtensorMap kvmap, const __grid_constant__ CUtensorMap qmap,
+                   const PParams p) {
+  using LY = Layout<D>;
+  constexpr int HALVES = D / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  const uint32_t bar0 = sb + LY::off_bar;
+  // barriers: q_full, kv_full[2], kv_empty[2], s_full[2], p_full, pv_done; then the TMEM address
+  const uint32_t q_full = bar0, kv_full = bar0 + 8, kv_empty = bar0 + 24, s_full = bar0 + 40,
+                 p_full = bar0 + 56, pv_done = bar0 + 64;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + LY::off_bar + 128);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int4 w0 = p.work[2 * blockIdx.x], w1 = p.work[2 * blockIdx.x + 1];
+  const int req = w0.x, q_row0 = w0.z, p0 = w0.w;
+  const int n_valid = w1.x, kvh = w1.y, n_tiles = w1.z;
+  const int last_key = p0 + n_valid - 1;  // the block's largest query position (< len)
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(kv_full + 8 * s, 1);
+      mbar_init(kv_empty + 8 * s, 1);
+      mbar_init(s_full + 8 * s, 1);
+    }
+    mbar_init(p_full, 4);
+    mbar_init(pv_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {  // TMEM: S0 [0,128), S1 [128,256), O [256, 256 + D)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ================================ TMA producer ================================
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kvmap)) : "memory");
+      uint64_t policy;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy));
+      const int g = p.group;
+      mbar_expect_tx(q_full, uint32_t(LY::Q));
+      for (int h = 0; h < HALVES; ++h)  // box {64, group heads, 1 half, 128/group rows}
+        tma_4d(sb + LY::off_q + h * kM * 128, &qmap, 0, kvh * g, h, q_row0, q_full);
+      const int tp = p.T < kN ? p.T : kN;  // tokens per TMA box
+      const int32_t* trow = p.table + int64_t(req) * p.table_stride;
+      for (int t = 0; t < n_tiles; ++t) {
+        const int s = t & 1;
+        mbar_wait(kv_empty + 8 * s, ((t >> 1) & 1) ^ 1);
+        const int tok0 = t * kN;
+        const int need = min(kN, last_key + 1 - tok0);
+        const int npc = (need + tp - 1) / tp;
+        mbar_expect_tx(kv_full + 8 * s, uint32_t(npc * tp * 128 * HALVES * 2));
+        const uint32_t kdst = sb + LY::off_kv + s * 2 * LY::TILE;
+        for (int k = 0; k < npc; ++k) {
+          const int tok = tok0 + k * tp;
+          const int c = __ldg(trow + tok / p.T);
+          const int cl = (c * p.L + p.layer) * 2;
+          for (int kv = 0; kv < 2; ++kv)
+            for (int h = 0; h < HALVES; ++h)
+              tma_5d(kdst + kv * LY::TILE + h * kN * 128 + k * tp * 128, &kvmap, 0, tok % p.T, h, kvh, cl + kv,
+                     kv_full + 8 * s, policy);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================ MMA issuer ================================
+    if (lane == 0) {
+      constexpr uint32_t id_s = idesc_bf16(kM, kN, false);
+      constexpr uint32_t id_pv = idesc_bf16(kM, D, true);
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int t) {
+        const int s = t & 1;
+        mbar_wait(kv_full + 8 * s, (t >> 1) & 1);
+        tc_fence_after();
+        const uint32_t kb = sb + LY::off_kv + s * 2 * LY::TILE;
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * (kM * 128) + (k & 3) * 32;
+          umma(tmem + s * 128, desc_sw128(sb + LY::off_q + off, 16), desc_sw128(kb + off, 16), id_s, k > 0);
+        }
+        umma_commit(s_full + 8 * s);
+      };
+      issue_s(0);
+      for (int t = 0; t < n_tiles; ++t) {
+        if (t + 1 < n_tiles) issue_s(t + 1);
+        mbar_wait(p_full, t & 1);
+        tc_fence_after();
+        const uint32_t vb = sb + LY::off_kv + (t & 1) * 2 * LY::TILE + LY::TILE;
+#pragma unroll
+        for (int k = 0; k < kN / 16; ++k)
+          umma(tmem + 256, desc_sw128(sb + LY::off_p + (k >> 2) * (kM * 128) + (k & 3) * 32, 16),
+               desc_sw128(vb + k * 2048, kN * 128), id_pv, (t > 0 || k > 0) ? 1u : 0u);
+        umma_commit(kv_empty + 8 * (t & 1));
+        umma_commit(pv_done);
+      }
+    }
+  } else {
+    // ================================ softmax ================================
+    const int quarter = warp & 3;           // TMEM lanes [32*quarter, 32*quarter + 32)
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16);
+    const int g = p.group;
+    const int pos_idx = row / g;
+    const bool valid = pos_idx < n_valid;
+    const int prow = valid ? p0 + pos_idx : p0;  // causal limit of this row
+    float m_run = -INFINITY, l_run = 0.f;
+    uint8_t* pbase = smem + LY::off_p + row * 128;
+    for (int t = 0; t < n_tiles; ++t) {
+      mbar_wait(s_full + 8 * (t & 1), (t >> 1) & 1);
+      tc_fence_after();
+      float x[kN];
+#pragma unroll
+      for (int c = 0; c < kN / 32; ++c) tmem_ld32(lane_addr + (t & 1) * 128 + c * 32, reinterpret_cast<uint32_t*>(x + 32 * c));
+      tmem_wait_ld();
+      const int lim = prow - t * kN;  // keys j <= lim of this tile are visible
+      float m_tile = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < kN; ++j) {
+        x[j] = j <= lim ? x[j] * p.scale_log2 : -INFINITY;
+        m_tile = fmaxf(m_tile, x[j]);
+      }
+      if (t > 0) mbar_wait(pv_done, (t - 1) & 1);  // P buffer free, O holds tiles < t
+      // lazy rescale: a row moves its reference max only when the tile max exceeds it by more
+      // than the headroom; the TMEM round trip of O is warp-uniform (tcgen05.ld/st are .aligned)
+      const bool grow = m_tile > m_run + kRescaleHeadroom;
+      if (t > 0 && __any_sync(0xffffffffu, grow)) {
+        const float alpha = grow ? ex2(m_run - m_tile) : 1.f;
+        l_run *= alpha;
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t o[32];
+          tmem_ld32(lane_addr + 256 + c * 32, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+          tmem_st32(lane_addr + 256 + c * 32, o);
+        }
+        tmem_wait_st();
+      }
+      if (grow) m_run = m_tile;
+      float sum = 0.f;
+#pragma unroll
+      for (int c16 = 0; c16 < kN / 8; ++c16) {  // 16-byte chunk = 8 tokens
+        float pv[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          pv[e] = ex2(x[c16 * 8 + e] - m_run);
+          sum += pv[e];
+        }
+        const int half = c16 >> 3, ch = c16 & 7;
+        uint4 v;
+        v.x = pack_bf16(pv[0], pv[1]);
+        v.y = pack_bf16(pv[2], pv[3]);
+        v.z = pack_bf16(pv[4], pv[5]);
+        v.w = pack_bf16(pv[6], pv[7]);
+        *reinterpret_cast<uint4*>(pbase + half * (kM * 128) + ((ch ^ (row & 7)) << 4)) = v;
+      }
+      l_run += sum;
+      if (t == n_tiles - 1) {  // V rows past the last visible key may hold anything: zero them
+        const int need = last_key + 1 - t * kN;
+        if (row >= need) {
+          uint8_t* vrow = smem + LY::off_kv + (t & 1) * 2 * LY::TILE + LY::TILE + row * 128;
+#pragma unroll
+          for (int h = 0; h < HALVES; ++h)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(vrow + h * kN * 128 + c * 16) = make_uint4(0, 0, 0, 0);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    // ---- epilogue: O / l -> bf16 -> out[q_row0 + pos][kvh*group + head][:] ----
+    mbar_wait(pv_done, (n_tiles - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l_run;
+    __nv_bfloat16* dst = p.out + (int64_t(q_row0 + pos_idx) * p.Hq + kvh * g + row % g) * D;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t o[32];
+      tmem_ld32(lane_addr + 256 + c * 32, o);
+      tmem_wait_ld();
+      if (valid) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 8) {
+          uint4 v;
+          v.x = pack_bf16(__uint_as_float(o[e + 0]) * inv, __uint_as_float(o[e + 1]) * inv);
+          v.y = pack_bf16(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
+          v.z = pack_bf16(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
+          v.w = pack_bf16(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
+          *reinterpret_cast<uint4*>(dst + c * 32 + e) = v;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+  }
+}
+
+template <int D>
+cudaError_t launch_d(const CUtensorMap& kvmap, const CUtensorMap& qmap, const PParams& prm, int n_work,
+                     cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Layout<D>::bytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  prefill_kernel<D><<<n_work, kThreads, Layout<D>::bytes, s>>>(kvmap, qmap, prm);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t encode_prefill_maps(CUtensorMap* kvmap, CUtensorMap* qmap, void* pool_base, int64_t max_chunks,
+                                const AttnShape& sh, const void* q, int64_t q_rows) {
+  const Driver& d = driver();
+  if (!d.ok) return cudaErrorNotSupported;
+  const int D = sh.D, halves = D / 64;
+  {  // pool: {64 d-elements, T tokens, d/64 halves, Hkv heads, chunk*L*2 + layer*2 + kv}
+    cuuint64_t dims[5] = {64, cuuint64_t(sh.T), cuuint64_t(halves), cuuint64_t(sh.Hkv),
+                          cuuint64_t(max_chunks) * sh.L * 2};
+    cuuint64_t strides[4] = {cuuint64_t(D) * 2, 128, cuuint64_t(sh.T) * D * 2, cuuint64_t(sh.Hkv) * sh.T * D * 2};
+    cuuint32_t box[5] = {64, cuuint32_t(sh.T < kN ? sh.T : kN), 1, 1, 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    if (d.tensorMapEncodeTiled(kvmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, pool_base, dims, strides, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  {  // q: {64 d-elements, Hq heads, d/64 halves, rows}; box = (group heads) x (128/group rows)
+    cuuint64_t dims[4] = {64, cuuint64_t(sh.Hq), cuuint64_t(halves), cuuint64_t(q_rows)};
+    cuuint64_t strides[3] = {cuuint64_t(D) * 2, 128, cuuint64_t(sh.Hq) * D * 2};
+    cuuint32_t box[4] = {64, cuuint32_t(sh.group), 1, cuuint32_t(kM / sh.group)};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (d.tensorMapEncodeTiled(qmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(q), dims, strides,
+                               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_prefill_attention(const CUtensorMap& kvmap, const CUtensorMap& qmap, const AttnShape& sh,
+                                     const int32_t* work, int32_t n_work, const int32_t* table,
+                                     int32_t table_stride, int32_t layer, void* out, float scale,
+                                     cudaStream_t s) {
+  PParams prm;
+  prm.work = reinterpret_cast<const int4*>(work);
+  prm.table = table;
+  prm.out = static_cast<__nv_bfloat16*>(out);
+  prm.table_stride = table_stride;
+  prm.Hq = sh.Hq;
+  prm.group = sh.group;
+  prm.T = sh.T;
+  prm.L = sh.L;
+  prm.layer = layer;
+  prm.scale_log2 = scale * 1.4426950408889634f;
+  if (n_work == 0) return cudaSuccess;
+  return sh.D == 128 ? launch_d<128>(kvmap, qmap, prm, n_work, s) : launch_d<64>(kvmap, qmap, prm, n_work, s);
+}
+
+}  // namespace ellm

@@ -78,6 +78,7 @@ _SIGS = {
     "ellm_set_swap_mode": (ctypes.c_int, [_P, _I32]),
     "ellm_set_vmm_overlap": (ctypes.c_int, [_P, ctypes.c_int64, _I32]),
     "ellm_vmm_sync": (ctypes.c_int, [_P]),
+    "ellm_prefill_attention": (ctypes.c_int, [_P, _I32, _I32, _P, _P, _P, _P, ctypes.c_float, _P]),
     "ellm_act_alloc": (ctypes.c_int, [_P, ctypes.c_int64, _P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_P)]),
     "ellm_act_free": (ctypes.c_int, [_P, ctypes.c_int64, _P]),
     "ellm_act_trim": (ctypes.c_int, [_P]),
@@ -240,6 +241,12 @@ class Pool:
 
     def vmm_sync(self) -> int:
         return ellm_vmm_sync(self._h)
+
+    def prefill_attention(self, layer, reqs, n_q, q, out, scale, stream=None) -> int:
+        """f4: causal attention of the last n_q[i] positions of each request (tcgen05)."""
+        r, nq = _i32(reqs), _i32(n_q)
+        return ellm_prefill_attention(self._h, int(layer), len(r), _ptr(r), _ptr(nq), _dptr(q), _dptr(out),
+                                      float(scale), _sptr(stream))
 
     # ---- f3: activation eTensors in the unified pool (P:310-325) ----
     def act_alloc(self, nbytes_or_chunks, stream=None, chunks=True):

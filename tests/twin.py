@@ -101,6 +101,41 @@ class Twin:
             check_attention(got, ref, f"layer {layer} reqs {list(reqs)[:8]}")
         return 0, (got, ref)
 
+    def prefill_q_bits(self, layer, reqs, n_q, rng):
+        """Queries for the last n_q positions of each request: N(0,1) rows, and on every other
+        position each head carries 2x the key of a random visible position (a logit gap of
+        ~2|k|^2/sqrt(d)), so a misplaced key or value moves the output by O(1). Needs needle=False
+        (the keys are regenerated here from the counter-based generator)."""
+        assert not self.needle
+        heads = np.arange(self.kv_head0, self.kv_head0 + self.Hkv)
+        out = []
+        for r, m in zip(reqs, n_q):
+            q = gen.f32_to_bf16(rng.standard_normal((m, self.Hq, self.d)).astype(np.float32))
+            for k in range(0, m, 2):
+                P = int(self.lens[r]) - m + k
+                if P < 0:
+                    break
+                j = int(rng.integers(0, P + 1))
+                kb = gen.kv_bits(self.seed, r, [j], layer, 0, heads, self.d, self.group, 0)[0]
+                k2 = gen.f32_to_bf16(2.0 * gen.bf16_to_f32(kb))
+                for h in range(self.Hq):
+                    q[k, h] = k2[h // self.group]
+            out.append(q)
+        return np.concatenate(out)
+
+    def prefill(self, layer, reqs, n_q, rng, check=True):
+        """Causal chunked-prefill attention (f4): oracle O12 vs the tcgen05 kernel."""
+        import torch
+        q = self.prefill_q_bits(layer, reqs, n_q, rng)
+        rc_o, ref = self.o.prefill_attention(layer, reqs, n_q, q, self.scale)
+        out = torch.full((q.shape[0], self.Hq, self.d), float("nan"), dtype=torch.bfloat16, device="cuda")
+        rc_p = self.p.prefill_attention(layer, reqs, n_q, bits_to_torch(q), out, self.scale)
+        torch.cuda.synchronize()
+        assert rc_o == rc_p, (rc_o, rc_p)
+        if rc_o == 0 and check:
+            return check_attention(torch_to_bits(out), ref, f"prefill layer {layer} reqs {list(reqs)[:8]}")
+        return rc_o
+
     def decode_fused(self, layer, reqs):
         """Oracle: append of the pending token + attention; product: the fused single launch."""
         import torch
