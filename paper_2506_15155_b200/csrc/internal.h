@@ -144,13 +144,19 @@ cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh,
                                    int32_t* arrivals, float scale, cudaStream_t s, int* launches);
 
 // chunked-prefill attention (prefill.cu). work: [n_work][8] int32 items
-// {req, len, q_row0, p0, n_valid, kvh, n_tiles, 0}.
-cudaError_t encode_prefill_maps(CUtensorMap* kvmap, CUtensorMap* qmap, void* pool_base, int64_t max_chunks,
-                                const AttnShape& sh, const void* q, int64_t q_rows);
-cudaError_t launch_prefill_attention(const CUtensorMap& kvmap, const CUtensorMap& qmap, const AttnShape& sh,
-                                     const int32_t* work, int32_t n_work, const int32_t* table,
-                                     int32_t table_stride, int32_t layer, void* out, float scale,
-                                     cudaStream_t s);
+// {req, len, q_row0, p0, n_valid, kvh, n_tiles, 0}. kv / run[] depend only on the pool (cached);
+// q is encoded per call.
+struct alignas(64) PrefillMaps {
+  CUtensorMap kv;       // 128-token boxes inside one chunk (T >= 128)
+  CUtensorMap run[4];   // boxes of 1/2/4/8 consecutive whole chunks (T < 128)
+  CUtensorMap q;
+};
+cudaError_t encode_prefill_kv_maps(PrefillMaps* m, void* pool_base, int64_t max_chunks, const AttnShape& sh,
+                                   int64_t chunk_bytes);
+cudaError_t encode_prefill_q_map(PrefillMaps* m, const AttnShape& sh, const void* q, int64_t q_rows);
+cudaError_t launch_prefill_attention(const PrefillMaps& maps, const AttnShape& sh, const int32_t* work,
+                                     int32_t n_work, const int32_t* table, int32_t table_stride, int32_t layer,
+                                     void* out, float scale, cudaStream_t s);
 
 }  // namespace ellm
 
@@ -259,6 +265,9 @@ struct ellm_pool {
   int64_t n_act_used = 0;
   std::vector<int32_t> unit_act;     // per unit: chunks inside live slots (under vmm_mu)
   std::vector<uint8_t> act_cached;   // per unit: kept mapped for activations (under vmm_mu)
+
+  ellm::PrefillMaps pf_maps{};       // f4 tensor maps over the pool (encoded on first use)
+  bool pf_ready = false;
 
   std::map<int32_t, std::pair<CUdeviceptr, size_t>> alias;
   int last_cuda_error = 0;

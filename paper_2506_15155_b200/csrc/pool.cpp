@@ -1315,10 +1315,15 @@ int ellm_prefill_attention(ellm_pool* p, int32_t layer, int32_t n, const int32_t
   const int32_t* d_work = nullptr;
   if (flat.size() * 4 > p->ring.seg_bytes()) return ELLM_ERR_UNSUPPORTED;  // > 32K work items
   if (int rc = upload_ints(p, flat, st, &d_work, nullptr)) return rc;
-  CUtensorMap kvmap, qmap;
-  cudaError_t e = encode_prefill_maps(&kvmap, &qmap, ellm_vtensor_base(p->vt), p->cfg.max_chunks, p->ash, q, rows);
-  if (e != cudaSuccess) return cuda_fail(p, e);
-  e = launch_prefill_attention(kvmap, qmap, p->ash, d_work, int32_t(items.size()), p->d_table,
+  cudaError_t e;
+  if (!p->pf_ready) {
+    if ((e = encode_prefill_kv_maps(&p->pf_maps, ellm_vtensor_base(p->vt), p->cfg.max_chunks, p->ash,
+                                    p->chunk_bytes)) != cudaSuccess)
+      return cuda_fail(p, e);
+    p->pf_ready = true;
+  }
+  if ((e = encode_prefill_q_map(&p->pf_maps, p->ash, q, rows)) != cudaSuccess) return cuda_fail(p, e);
+  e = launch_prefill_attention(p->pf_maps, p->ash, d_work, int32_t(items.size()), p->d_table,
                                p->cfg.max_chunks_per_request, layer, out, scale, st);
   if (e != cudaSuccess) return cuda_fail(p, e);
   ++p->launches;

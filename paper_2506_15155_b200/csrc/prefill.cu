@@ -39,11 +39,11 @@ template <int D>
 struct Layout {
   static constexpr int TILE = kN * D * 2;  // one K or V tile: [D/64][128 tokens][64] bf16
   static constexpr int Q = kM * D * 2;     // [D/64][128 rows][64]
-  static constexpr int P = kM * kN * 2;    // [2 token halves][128 rows][64]
+  static constexpr int P = kM * kN * 2;    // one P buffer: [2 token halves][128 rows][64]
   static constexpr int off_q = 0;
   static constexpr int off_kv = Q;         // stage s: K at off_kv + 2*s*TILE, V at + TILE
   static constexpr int off_p = off_kv + kStages * 2 * TILE;
-  static constexpr int off_bar = off_p + P;
+  static constexpr int off_bar = off_p + 2 * P;  // P double-buffered
   // >= 116 KB so one CTA owns an SM (its 512 TMEM columns are the whole TMEM)
   static constexpr int bytes = (off_bar + 256 + 1024) > 118784 ? (off_bar + 256 + 1024) : 118784;
 };
@@ -155,23 +155,25 @@ struct PParams {
   const int4* work;        // [n_work][2]: {req, len, q_row0, p0}, {n_valid, kvh, n_tiles, 0}
   const int32_t* table;
   __nv_bfloat16* out;      // [rows][Hq][D]
-  int32_t table_stride, Hq, group, T, L, layer;
+  int32_t table_stride, Hq, group, T, L, layer, Hkv;
   float scale_log2;
 };
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
-    prefill_kernel(const __grid_constant__ CUtensorMap kvmap, const __grid_constant__ CUtensorMap qmap,
-                   const PParams p) {
+    prefill_kernel(const __grid_constant__ PrefillMaps maps, const PParams p) {
   using LY = Layout<D>;
   constexpr int HALVES = D / 64;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sb = smem_u32(smem);
   const uint32_t bar0 = sb + LY::off_bar;
-  // barriers: q_full, kv_full[2], kv_empty[2], s_full[2], p_full, pv_done; then the TMEM address
-  const uint32_t q_full = bar0, kv_full = bar0 + 8, kv_empty = bar0 + 24, s_full = bar0 + 40,
-                 p_full = bar0 + 56, pv_done = bar0 + 64;
+  // barriers: q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2],
+  // pv_done[2]; then the TMEM address. K and V slots are released separately (K(t) right after
+  // S(t)); P is double-buffered, so the softmax of tile t+1 overlaps P.V of tile t and waits for
+  // it only when it must rescale O.
+  const uint32_t q_full = bar0, k_full = bar0 + 8, k_empty = bar0 + 24, v_full = bar0 + 40,
+                 v_empty = bar0 + 56, s_full = bar0 + 72, p_full = bar0 + 88, pv_done = bar0 + 104;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + LY::off_bar + 128);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -183,12 +185,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(kv_full + 8 * s, 1);
-      mbar_init(kv_empty + 8 * s, 1);
+      mbar_init(k_full + 8 * s, 1);
+      mbar_init(k_empty + 8 * s, 1);
+      mbar_init(v_full + 8 * s, 1);
+      mbar_init(v_empty + 8 * s, 1);
       mbar_init(s_full + 8 * s, 1);
+      mbar_init(p_full + 8 * s, 4);
+      mbar_init(pv_done + 8 * s, 1);
     }
-    mbar_init(p_full, 4);
-    mbar_init(pv_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -205,34 +209,67 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ================================ TMA producer ================================
+    // The whole warp walks the chunk table (lane k: piece k of a tile, loaded one tile ahead so
+    // the load latency hides behind the barrier waits); lane 0 issues the TMAs.
+    uint64_t policy;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy));
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kvmap)) : "memory");
-      uint64_t policy;
-      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy));
-      const int g = p.group;
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.kv)) : "memory");
       mbar_expect_tx(q_full, uint32_t(LY::Q));
       for (int h = 0; h < HALVES; ++h)  // box {64, group heads, 1 half, 128/group rows}
-        tma_4d(sb + LY::off_q + h * kM * 128, &qmap, 0, kvh * g, h, q_row0, q_full);
-      const int tp = p.T < kN ? p.T : kN;  // tokens per TMA box
-      const int32_t* trow = p.table + int64_t(req) * p.table_stride;
-      for (int t = 0; t < n_tiles; ++t) {
-        const int s = t & 1;
-        mbar_wait(kv_empty + 8 * s, ((t >> 1) & 1) ^ 1);
-        const int tok0 = t * kN;
-        const int need = min(kN, last_key + 1 - tok0);
-        const int npc = (need + tp - 1) / tp;
-        mbar_expect_tx(kv_full + 8 * s, uint32_t(npc * tp * 128 * HALVES * 2));
-        const uint32_t kdst = sb + LY::off_kv + s * 2 * LY::TILE;
-        for (int k = 0; k < npc; ++k) {
-          const int tok = tok0 + k * tp;
-          const int c = __ldg(trow + tok / p.T);
-          const int cl = (c * p.L + p.layer) * 2;
-          for (int kv = 0; kv < 2; ++kv)
+        tma_4d(sb + LY::off_q + h * kM * 128, &maps.q, 0, kvh * p.group, h, q_row0, q_full);
+    }
+    const int tp = p.T < kN ? p.T : kN;  // tokens per chunk piece
+    const int32_t* trow = p.table + int64_t(req) * p.table_stride;
+    auto pieces = [&](int t) { return (min(kN, last_key + 1 - t * kN) + tp - 1) / tp; };
+    auto load_ent = [&](int t) {
+      return (t < n_tiles && lane < pieces(t)) ? __ldg(trow + (t * kN + lane * tp) / p.T) : -1;
+    };
+    // order: K(0), K(1), V(0), K(2), V(1), ... — K runs one tile ahead of V
+    auto issue = [&](int t, int kv, int e) {
+      const int s = t & 1;
+      const uint32_t full = (kv ? v_full : k_full) + 8 * s, empty = (kv ? v_empty : k_empty) + 8 * s;
+      const int npc = pieces(t);
+      const uint32_t dst = sb + LY::off_kv + s * 2 * LY::TILE + kv * LY::TILE;
+      // runs of consecutive chunk ids go as one box of 1/2/4/8 chunks (TMA issue cost is per box)
+      const int prev = __shfl_up_sync(0xffffffffu, e, 1);
+      unsigned starts = __ballot_sync(0xffffffffu, lane < npc && (lane == 0 || e != prev + 1 || p.T >= kN));
+      if (lane == 0) {
+        mbar_wait(empty, ((t >> 1) & 1) ^ 1);
+        mbar_expect_tx(full, uint32_t(npc * tp * 128 * HALVES));
+      }
+      const int lh = (p.layer * 2 + kv) * p.Hkv + kvh;
+      while (starts) {
+        const int k = __ffs(starts) - 1;
+        starts &= starts - 1;
+        const int kend = starts ? __ffs(starts) - 1 : npc;
+        const int c = __shfl_sync(0xffffffffu, e, k);
+        if (lane == 0) {
+          if (p.T >= kN) {  // one 128-token box inside one chunk
             for (int h = 0; h < HALVES; ++h)
-              tma_5d(kdst + kv * LY::TILE + h * kN * 128 + k * tp * 128, &kvmap, 0, tok % p.T, h, kvh, cl + kv,
-                     kv_full + 8 * s, policy);
+              tma_5d(dst + h * kN * 128, &maps.kv, 0, (t * kN) % p.T, h, kvh, (c * p.L + p.layer) * 2 + kv, full,
+                     policy);
+          } else {
+            for (int done = 0; done < kend - k;) {
+              const int lg = min(3, 31 - __clz(kend - k - done));
+              for (int h = 0; h < HALVES; ++h)
+                tma_5d(dst + h * kN * 128 + (k + done) * tp * 128, &maps.run[lg], 0, 0, h, lh, c + done, full,
+                       policy);
+              done += 1 << lg;
+            }
+          }
         }
       }
+      __syncwarp();
+    };
+    int e_cur = load_ent(0), e_next = load_ent(1);
+    issue(0, 0, e_cur);
+    for (int t = 0; t < n_tiles; ++t) {
+      const int e_after = load_ent(t + 2);  // in flight while this iteration waits
+      if (t + 1 < n_tiles) issue(t + 1, 0, e_next);
+      issue(t, 1, e_cur);
+      e_cur = e_next;
+      e_next = e_after;
     }
   } else if (warp == 1) {
     // ================================ MMA issuer ================================
@@ -242,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(q_full, 0);
       auto issue_s = [&](int t) {
         const int s = t & 1;
-        mbar_wait(kv_full + 8 * s, (t >> 1) & 1);
+        mbar_wait(k_full + 8 * s, (t >> 1) & 1);
         tc_fence_after();
         const uint32_t kb = sb + LY::off_kv + s * 2 * LY::TILE;
 #pragma unroll
@@ -251,19 +288,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma(tmem + s * 128, desc_sw128(sb + LY::off_q + off, 16), desc_sw128(kb + off, 16), id_s, k > 0);
         }
         umma_commit(s_full + 8 * s);
+        umma_commit(k_empty + 8 * s);
       };
       issue_s(0);
       for (int t = 0; t < n_tiles; ++t) {
         if (t + 1 < n_tiles) issue_s(t + 1);
-        mbar_wait(p_full, t & 1);
+        mbar_wait(p_full + 8 * (t & 1), (t >> 1) & 1);
+        mbar_wait(v_full + 8 * (t & 1), (t >> 1) & 1);
         tc_fence_after();
         const uint32_t vb = sb + LY::off_kv + (t & 1) * 2 * LY::TILE + LY::TILE;
 #pragma unroll
         for (int k = 0; k < kN / 16; ++k)
-          umma(tmem + 256, desc_sw128(sb + LY::off_p + (k >> 2) * (kM * 128) + (k & 3) * 32, 16),
+          umma(tmem + 256, desc_sw128(sb + LY::off_p + (t & 1) * LY::P + (k >> 2) * (kM * 128) + (k & 3) * 32, 16),
                desc_sw128(vb + k * 2048, kN * 128), id_pv, (t > 0 || k > 0) ? 1u : 0u);
-        umma_commit(kv_empty + 8 * (t & 1));
-        umma_commit(pv_done);
+        umma_commit(v_empty + 8 * (t & 1));
+        umma_commit(pv_done + 8 * (t & 1));
       }
     }
   } else {
@@ -276,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool valid = pos_idx < n_valid;
     const int prow = valid ? p0 + pos_idx : p0;  // causal limit of this row
     float m_run = -INFINITY, l_run = 0.f;
-    uint8_t* pbase = smem + LY::off_p + row * 128;
+    uint8_t* prow_base = smem + LY::off_p + row * 128;
     for (int t = 0; t < n_tiles; ++t) {
       mbar_wait(s_full + 8 * (t & 1), (t >> 1) & 1);
       tc_fence_after();
@@ -285,17 +324,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = 0; c < kN / 32; ++c) tmem_ld32(lane_addr + (t & 1) * 128 + c * 32, reinterpret_cast<uint32_t*>(x + 32 * c));
       tmem_wait_ld();
       const int lim = prow - t * kN;  // keys j <= lim of this tile are visible
-      float m_tile = -INFINITY;
+      if (!__all_sync(0xffffffffu, lim >= kN - 1)) {  // diagonal / last tiles only
 #pragma unroll
-      for (int j = 0; j < kN; ++j) {
-        x[j] = j <= lim ? x[j] * p.scale_log2 : -INFINITY;
-        m_tile = fmaxf(m_tile, x[j]);
+        for (int j = 0; j < kN; ++j)
+          if (j > lim) x[j] = -INFINITY;
       }
-      if (t > 0) mbar_wait(pv_done, (t - 1) & 1);  // P buffer free, O holds tiles < t
+      // row max of the raw scores with 8 independent chains (scale > 0 commutes with max)
+      float mx[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx[i] = x[i];
+#pragma unroll
+      for (int j = 8; j < kN; ++j) mx[j & 7] = fmaxf(mx[j & 7], x[j]);
+      const float m_tile =
+          fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) *
+          p.scale_log2;
       // lazy rescale: a row moves its reference max only when the tile max exceeds it by more
       // than the headroom; the TMEM round trip of O is warp-uniform (tcgen05.ld/st are .aligned)
+      // and needs P.V of tile t-1 complete
       const bool grow = m_tile > m_run + kRescaleHeadroom;
       if (t > 0 && __any_sync(0xffffffffu, grow)) {
+        mbar_wait(pv_done + 8 * ((t - 1) & 1), ((t - 1) >> 1) & 1);
         const float alpha = grow ? ex2(m_run - m_tile) : 1.f;
         l_run *= alpha;
         tc_fence_after();
@@ -311,14 +359,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_wait_st();
       }
       if (grow) m_run = m_tile;
-      float sum = 0.f;
+      if (t >= 2) mbar_wait(pv_done + 8 * (t & 1), ((t >> 1) - 1) & 1);  // P buffer of tile t-2 read
+      uint8_t* pbase = prow_base + (t & 1) * LY::P;
+      float sm[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 independent partial sums
+      const float neg_m = -m_run;
 #pragma unroll
       for (int c16 = 0; c16 < kN / 8; ++c16) {  // 16-byte chunk = 8 tokens
         float pv[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          pv[e] = ex2(x[c16 * 8 + e] - m_run);
-          sum += pv[e];
+          pv[e] = ex2(fmaf(x[c16 * 8 + e], p.scale_log2, neg_m));
+          sm[e] += pv[e];
         }
         const int half = c16 >> 3, ch = c16 & 7;
         uint4 v;
@@ -328,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         v.w = pack_bf16(pv[6], pv[7]);
         *reinterpret_cast<uint4*>(pbase + half * (kM * 128) + ((ch ^ (row & 7)) << 4)) = v;
       }
-      l_run += sum;
+      l_run += ((sm[0] + sm[1]) + (sm[2] + sm[3])) + ((sm[4] + sm[5]) + (sm[6] + sm[7]));
       if (t == n_tiles - 1) {  // V rows past the last visible key may hold anything: zero them
         const int need = last_key + 1 - t * kN;
         if (row >= need) {
@@ -342,10 +393,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(p_full + 8 * (t & 1));
     }
     // ---- epilogue: O / l -> bf16 -> out[q_row0 + pos][kvh*group + head][:] ----
-    mbar_wait(pv_done, (n_tiles - 1) & 1);
+    mbar_wait(pv_done + 8 * ((n_tiles - 1) & 1), ((n_tiles - 1) >> 1) & 1);
     tc_fence_after();
     const float inv = 1.f / l_run;
     __nv_bfloat16* dst = p.out + (int64_t(q_row0 + pos_idx) * p.Hq + kvh * g + row % g) * D;
@@ -376,8 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 template <int D>
-cudaError_t launch_d(const CUtensorMap& kvmap, const CUtensorMap& qmap, const PParams& prm, int n_work,
-                     cudaStream_t s) {
+cudaError_t launch_d(const PrefillMaps& maps, const PParams& prm, int n_work, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(prefill_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -385,43 +435,59 @@ cudaError_t launch_d(const CUtensorMap& kvmap, const CUtensorMap& qmap, const PP
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  prefill_kernel<D><<<n_work, kThreads, Layout<D>::bytes, s>>>(kvmap, qmap, prm);
+  prefill_kernel<D><<<n_work, kThreads, Layout<D>::bytes, s>>>(maps, prm);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t encode_prefill_maps(CUtensorMap* kvmap, CUtensorMap* qmap, void* pool_base, int64_t max_chunks,
-                                const AttnShape& sh, const void* q, int64_t q_rows) {
+cudaError_t encode_prefill_kv_maps(PrefillMaps* m, void* pool_base, int64_t max_chunks, const AttnShape& sh,
+                                   int64_t chunk_bytes) {
   const Driver& d = driver();
   if (!d.ok) return cudaErrorNotSupported;
   const int D = sh.D, halves = D / 64;
-  {  // pool: {64 d-elements, T tokens, d/64 halves, Hkv heads, chunk*L*2 + layer*2 + kv}
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  {  // {64 d-elements, T tokens, d/64 halves, Hkv heads, chunk*L*2 + layer*2 + kv}; box 128 tokens
     cuuint64_t dims[5] = {64, cuuint64_t(sh.T), cuuint64_t(halves), cuuint64_t(sh.Hkv),
                           cuuint64_t(max_chunks) * sh.L * 2};
     cuuint64_t strides[4] = {cuuint64_t(D) * 2, 128, cuuint64_t(sh.T) * D * 2, cuuint64_t(sh.Hkv) * sh.T * D * 2};
     cuuint32_t box[5] = {64, cuuint32_t(sh.T < kN ? sh.T : kN), 1, 1, 1};
-    cuuint32_t es[5] = {1, 1, 1, 1, 1};
-    if (d.tensorMapEncodeTiled(kvmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, pool_base, dims, strides, box, es,
+    if (d.tensorMapEncodeTiled(&m->kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, pool_base, dims, strides, box, es,
                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  {  // q: {64 d-elements, Hq heads, d/64 halves, rows}; box = (group heads) x (128/group rows)
-    cuuint64_t dims[4] = {64, cuuint64_t(sh.Hq), cuuint64_t(halves), cuuint64_t(q_rows)};
-    cuuint64_t strides[3] = {cuuint64_t(D) * 2, 128, cuuint64_t(sh.Hq) * D * 2};
-    cuuint32_t box[4] = {64, cuuint32_t(sh.group), 1, cuuint32_t(kM / sh.group)};
-    cuuint32_t es[4] = {1, 1, 1, 1};
-    if (d.tensorMapEncodeTiled(qmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(q), dims, strides,
-                               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  // runs of consecutive chunks: {64, T, d/64, (layer*2 + kv)*Hkv + head, chunk}; box 1/2/4/8 chunks
+  for (int lg = 0; lg < 4; ++lg) {
+    cuuint64_t dims[5] = {64, cuuint64_t(sh.T), cuuint64_t(halves), cuuint64_t(sh.L) * 2 * sh.Hkv,
+                          cuuint64_t(max_chunks)};
+    cuuint64_t strides[4] = {cuuint64_t(D) * 2, 128, cuuint64_t(sh.T) * D * 2, cuuint64_t(chunk_bytes)};
+    cuuint32_t box[5] = {64, cuuint32_t(sh.T < kN ? sh.T : kN), 1, 1, cuuint32_t(1) << lg};
+    if (d.tensorMapEncodeTiled(&m->run[lg], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, pool_base, dims, strides, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
   return cudaSuccess;
 }
 
-cudaError_t launch_prefill_attention(const CUtensorMap& kvmap, const CUtensorMap& qmap, const AttnShape& sh,
-                                     const int32_t* work, int32_t n_work, const int32_t* table,
+cudaError_t encode_prefill_q_map(PrefillMaps* m, const AttnShape& sh, const void* q, int64_t q_rows) {
+  const Driver& d = driver();
+  if (!d.ok) return cudaErrorNotSupported;
+  const int D = sh.D, halves = D / 64;
+  // q: {64 d-elements, Hq heads, d/64 halves, rows}; box = (group heads) x (128/group rows)
+  cuuint64_t dims[4] = {64, cuuint64_t(sh.Hq), cuuint64_t(halves), cuuint64_t(q_rows)};
+  cuuint64_t strides[3] = {cuuint64_t(D) * 2, 128, cuuint64_t(sh.Hq) * D * 2};
+  cuuint32_t box[4] = {64, cuuint32_t(sh.group), 1, cuuint32_t(kM / sh.group)};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  if (d.tensorMapEncodeTiled(&m->q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(q), dims, strides, box,
+                             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  return cudaSuccess;
+}
+
+cudaError_t launch_prefill_attention(const PrefillMaps& maps, const AttnShape& sh, const int32_t* work, int32_t n_work, const int32_t* table,
                                      int32_t table_stride, int32_t layer, void* out, float scale,
                                      cudaStream_t s) {
   PParams prm;
@@ -432,11 +498,12 @@ cudaError_t launch_prefill_attention(const CUtensorMap& kvmap, const CUtensorMap
   prm.Hq = sh.Hq;
   prm.group = sh.group;
   prm.T = sh.T;
+  prm.Hkv = sh.Hkv;
   prm.L = sh.L;
   prm.layer = layer;
   prm.scale_log2 = scale * 1.4426950408889634f;
   if (n_work == 0) return cudaSuccess;
-  return sh.D == 128 ? launch_d<128>(kvmap, qmap, prm, n_work, s) : launch_d<64>(kvmap, qmap, prm, n_work, s);
+  return sh.D == 128 ? launch_d<128>(maps, prm, n_work, s) : launch_d<64>(maps, prm, n_work, s);
 }
 
 }  // namespace ellm

@@ -60,3 +60,19 @@ def test_prefill_errors_match_oracle():
     assert rc == 0
     assert t.prefill(0, [0, 1], [4, 4], rng) == -5
     t.prefill(0, [0], [100], rng)
+
+
+def test_prefill_fragmented_tables():
+    """Chunk ids of a request in runs of 1..9 (two requests reserving alternately): the producer
+    splits each 128-key tile into boxes of 1/2/4/8 consecutive chunks."""
+    rng = np.random.default_rng(12)
+    t = Twin(1, 32, 8, 128, 16, 400, 400, 2, 200, 0, seed=8, needle=False)
+    for _ in range(30):
+        for r in (0, 1):
+            n = 16 * int(rng.integers(1, 10)) - int(rng.integers(0, 3))
+            if t.reserve([r], [n]) == 0:
+                t.append_all_layers([r], [n])
+    runs = np.diff(t.o.table(0)[0]) == 1
+    assert runs.any() and not runs.all()
+    lens = [int(t.lens[0]), int(t.lens[1])]
+    t.prefill(0, [0, 1], [lens[0], min(lens[1], 333)], rng)
