@@ -462,6 +462,33 @@ def main():
     assert pool.set_vmm_overlap(0, False) == ellm.OK and pool.vmm_sync() == ellm.OK
     torch.cuda.synchronize()
 
+    # ---- f4: chunked-prefill attention (tcgen05) over the same chunk-mapped KV: the last
+    #      PF_NQ positions of PF_B requests attend causally to their whole context ----
+    PF_B, PF_NQ, PF_ITERS = 4, 2048, 5
+    pf_reqs = list(range(min(PF_B, B)))
+    pf_len = [int(pool.table(r)[1]) for r in pf_reqs]
+    qg = torch.Generator(device="cuda").manual_seed(11)
+    pf_q = torch.randn((len(pf_reqs) * PF_NQ, wl.hq_local, wl.head_dim), generator=qg, device="cuda",
+                       dtype=torch.bfloat16)
+    pf_out = torch.empty_like(pf_q)
+    assert pool.prefill_attention(0, pf_reqs, [PF_NQ] * len(pf_reqs), pf_q, pf_out, scale, sp) == ellm.OK
+    p0e, p1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0e.record(stream)
+    for it in range(PF_ITERS):
+        pool.prefill_attention(it % L, pf_reqs, [PF_NQ] * len(pf_reqs), pf_q, pf_out, scale, sp)
+    p1e.record(stream)
+    torch.cuda.synchronize()
+    pf_ms = p0e.elapsed_time(p1e) / PF_ITERS
+    pf_keys = sum(sum(n - PF_NQ + i + 1 for i in range(PF_NQ)) for n in pf_len)
+    pf_flops = 4.0 * wl.head_dim * pf_keys * wl.hq_local
+    mp_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    bf16_peak = json.load(open(mp_path)).get("bf16_tflops") if os.path.exists(mp_path) else None
+    f4 = {"requests": len(pf_reqs), "n_q": PF_NQ, "context": pf_len[0], "ms": round(pf_ms, 3),
+          "tflops": round(pf_flops / pf_ms / 1e9, 1),
+          "frac_of_bf16_peak": round(pf_flops / pf_ms / 1e9 / bf16_peak, 3) if bf16_peak else None,
+          "flops": "4*d*sum_i(P_i+1)*Hq (causal, algorithmic)", "peak_source": "MEASURED_PEAKS.json bf16_tflops"}
+    del pf_q, pf_out
+
     rows = {
         "a1_pool_create": {"s": round(t_create, 3), "chunks_mapped": st_create["n_map"],
                            "map_us_per_chunk": round(st_create["map_ns"] / max(1, st_create["n_map"]) / 1e3, 2),
@@ -476,6 +503,7 @@ def main():
                                 "unmap_us_per_chunk": round((st1["unmap_ns"] - st0["unmap_ns"]) / max(1, n_vmm) / 1e3, 2),
                                 "map_us_per_chunk": round((st1["map_ns"] - st0["map_ns"]) / max(1, n_vmm) / 1e3, 2)},
         "f1_vmm_overlap": f1,
+        "f4_prefill": f4,
     }
 
     cpu = None
