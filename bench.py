@@ -39,6 +39,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ellm", "reference"], default="ellm")
     ap.add_argument("--workload", choices=["c2", "c4"], default="c2")
+    ap.add_argument("--gather", choices=["p2p", "nccl"], default="p2p",
+                    help="N>1 head gather: fused into the attention epilogue over peer memory (p2p) "
+                         "or a separate NCCL all-gather per layer")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="override the workload's request count (testing; the JSON config records it)")
     ap.add_argument("--no-swap", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -215,12 +220,22 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # ELLM_BENCH_SAME_GPU=1 (testing on a 1-GPU box): every rank on cuda:0, gloo process group;
+    # the p2p gather then runs over CUDA IPC on one device instead of NVLink.
+    same_gpu = os.environ.get("ELLM_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     wl = W.c2(world, rank) if args.workload == "c2" else W.c4(world, rank)
+    if args.batch:
+        wl.batch = args.batch
     B, L = wl.batch, wl.n_layers
     swap_chunks = 1024 if not args.no_swap else 0
     t_create = time.perf_counter()
@@ -248,8 +263,14 @@ def main():
     for s in range(n_steps + e2e_steps):
         inputs.append(W.decode_inputs(wl, s, lens + s))
     out = torch.empty((L, B, wl.hq_local, wl.head_dim), dtype=torch.bfloat16, device="cuda")
+    p2p = world > 1 and args.gather == "p2p"
     gath = torch.empty((L, world, B, wl.hq_local, wl.head_dim), dtype=torch.bfloat16, device="cuda") \
-        if world > 1 else None
+        if world > 1 and not p2p else None
+    pg = None
+    if p2p:  # a10 fused: every rank's attention stores its heads' rows into all ranks' windows
+        from paper_2506_15155_b200 import shard
+        pg = shard.PeerGather(pool, world, rank, wl.n_heads_q, L, B, wl.head_dim, device=local)
+        dist.barrier()
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
     attn_ev, app_ev, reserve_s = [], [], []
@@ -266,7 +287,10 @@ def main():
                 if record:
                     e0 = torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
-                rc = pool.decode_append_attention(l, reqs, k[l], v[l], q[l], out[l], scale, sp)
+                if pg is not None:  # ... + the head gather (a10) in the same launch
+                    rc = pool.attention_gather(l, reqs, q[l], pg.offset(l), scale, k[l], v[l], sp)
+                else:
+                    rc = pool.decode_append_attention(l, reqs, k[l], v[l], q[l], out[l], scale, sp)
                 if rc:
                     raise ellm.EllmError(rc, "decode_append_attention")
             else:
@@ -280,14 +304,21 @@ def main():
                     e0 = torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
                     app_ev.append((a0, e0))
-                rc = pool.attention(l, reqs, q[l], out[l], scale, sp)
+                if pg is not None:
+                    rc = pool.attention_gather(l, reqs, q[l], pg.offset(l), scale, None, None, sp)
+                else:
+                    rc = pool.attention(l, reqs, q[l], out[l], scale, sp)
                 if rc:
                     raise ellm.EllmError(rc, "attention")
             if record:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(stream)
                 attn_ev.append((e0, e1))
-            if gath is not None:
+            if pg is not None:  # the layer's consumer waits for every rank's rows
+                rc = pool.gather_wait(l, sp)
+                if rc:
+                    raise ellm.EllmError(rc, "gather_wait")
+            elif gath is not None:
                 dist.all_gather_into_tensor(gath[l], out[l])
 
     def barrier():
@@ -316,7 +347,7 @@ def main():
     el_ms = ev0.elapsed_time(ev1)
     attn_ms = [a.elapsed_time(b) for a, b in attn_ev]
     if dist:
-        t = torch.tensor([el_ms, statistics.mean(attn_ms)], device="cuda")
+        t = torch.tensor([el_ms, statistics.mean(attn_ms)], device="cpu" if same_gpu else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         el_ms, attn_mean = float(t[0]), float(t[1])
     else:
@@ -333,7 +364,7 @@ def main():
     peak, peak_src = hbm_peak()
     traffic = None
     tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and world == 1 and not args.batch:  # captured for the N=1 workload only
         try:
             traffic = json.load(open(tp)).get(wl.name)
         except Exception:
@@ -352,7 +383,10 @@ def main():
         for s in range(n_steps, n_steps + n_e2e):
             hin.append(tuple(x.cpu().pin_memory() for x in inputs[s]))
         dq, dk, dv = (torch.empty_like(x) for x in inputs[0])
-        hout = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        if pg is not None:  # the result of a step is the gathered [L, B, Hq, d] output
+            hout = torch.empty(L * pg.stride, dtype=torch.uint8).pin_memory()
+        else:
+            hout = torch.empty(out.shape, dtype=out.dtype).pin_memory()
         h2d = sum(x.numel() * x.element_size() for x in hin[0])
         d2h = hout.numel() * hout.element_size()
         barrier()
@@ -363,12 +397,15 @@ def main():
             dk.copy_(hk, non_blocking=True)
             dv.copy_(hv, non_blocking=True)
             step(dq, dk, dv)
-            hout.copy_(out, non_blocking=True)
+            if pg is not None:
+                ellm.memcpy_async(hout.data_ptr(), pg.out(0), d2h, sp)
+            else:
+                hout.copy_(out, non_blocking=True)
         e1.record(stream)
         barrier()
         ems = e0.elapsed_time(e1)
         if dist:
-            t = torch.tensor([ems], device="cuda")
+            t = torch.tensor([ems], device="cpu" if same_gpu else "cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t[0])
         e2e = {"value": round(B * n_e2e / (ems / 1e3), 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
@@ -516,11 +553,18 @@ def main():
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (seeded counter-based generator, 3 needles per request/layer/kv-head)",
-                "config": workload_config(wl, world), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "config": {**workload_config(wl, world),
+                           **({"gather": "fused attention epilogue, P2P stores into every rank's window"
+                               if pg is not None else "NCCL all_gather_into_tensor per layer"} if world > 1 else {})},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk.summary(),
                 "attention_gbs": round(achieved, 1), "attention_frac_of_peak": roof["frac"], "swap": swap,
                 "rows": rows}
         print(json.dumps(line), flush=True)
+    if pg is not None:
+        barrier()  # no rank unmaps its peers' windows while one may still write
+        pg.close()
+        barrier()
     pool.close()
     if dist:
         dist.destroy_process_group()

@@ -275,6 +275,49 @@ int ellm_torch_set_pool(ellm_pool* pool);
 void* ellm_torch_alloc(size_t size, int device, void* stream);
 void ellm_torch_free(void* ptr, size_t size, int device, void* stream);
 
+/* ---- a10: head-sharded output gather fused into attention ------
+ * KV-head sharding over N GPUs of one box: rank i owns kv-heads [i*Hkv/N, (i+1)*Hkv/N) and
+ * q-heads [i*Hq/N, (i+1)*Hq/N) (its pool is created with the local counts). After attention
+ * every rank needs all N ranks' head outputs. Instead of attention followed by an all-gather,
+ * the attention kernel's split-K merge stores each finished output row directly into EVERY
+ * rank's gather window over peer memory (NVLink P2P stores), and each CTA then adds the number
+ * of requests it merged to every rank's flag word for that layer (release, system scope).
+ * A gather window is one device allocation per rank, identical size on all ranks:
+ *   [0, ELLM_GATHER_DATA_OFFSET)     uint32 flag words, one per layer (monotone counters)
+ *   [ELLM_GATHER_DATA_OFFSET, bytes) rows: a call with out_offset writes [n, Hq_total, d] bf16
+ *                                     at data + out_offset (global q-head order).
+ * window_create: cudaMalloc + zero on `device` (makes it the calling thread's current device);
+ *   ipc_handle_out (optional, 64 B) receives its cudaIpcMemHandle_t for the other ranks.
+ * ipc_open / ipc_close: map / unmap another process's window (cudaIpcOpenMemHandle, lazy peer
+ *   access). The caller owns windows and opened mappings; they must outlive the attachment.
+ * gather_attach: windows[i] = rank i's window as seen from this process (own window at
+ *   windows[rank]); heads_q_total must equal world * the pool's Hq (INVALID_ARG), world in
+ *   [1, 8] and rank < world (OUT_OF_RANGE), windows 256-B aligned and non-NULL. Reads this
+ *   rank's current flag values: all ranks must be idle (attach everywhere, then a barrier).
+ * attention_gather: paged_decode_attention (k_new == v_new == NULL) or decode_append_attention
+ *   (both given; same preconditions and errors as those calls) whose output goes to every
+ *   rank's window at out_offset (16-B aligned; past the window -> OUT_OF_RANGE; not attached ->
+ *   INVALID_ARG). Every rank must issue the same sequence of calls with the same requests.
+ * gather_wait: makes `stream` wait until this rank's flag word of `layer` shows every rank's
+ *   rows of all attention_gather calls issued so far for that layer (one 1-thread kernel;
+ *   after ELLM_GATHER_TIMEOUT_MS, default 20000, it traps: a missing peer fails the stream
+ *   with ELLM_ERR_CUDA instead of hanging it). Window rows of one layer may be rewritten by the
+ *   next call for that layer only after every rank has consumed them (the caller's order). */
+#define ELLM_GATHER_DATA_OFFSET 4096
+int ellm_gather_window_create(int32_t device, int64_t bytes, void** window_out, void* ipc_handle_out);
+int ellm_gather_window_destroy(void* window);
+int ellm_ipc_open(const void* ipc_handle, void** window_out);
+int ellm_ipc_close(void* window);
+int ellm_gather_attach(ellm_pool* pool, int32_t world, int32_t rank, int32_t heads_q_total,
+                       void* const* windows, int64_t window_bytes);
+int ellm_gather_detach(ellm_pool* pool);
+int ellm_attention_gather(ellm_pool* pool, int32_t layer, int32_t n, const int32_t* req_ids,
+                          const void* k_new, const void* v_new, const void* q, int64_t out_offset,
+                          float softmax_scale, void* stream);
+int ellm_gather_wait(ellm_pool* pool, int32_t layer, void* stream);
+/* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream): host <-> window copies. */
+int ellm_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
+
 /* Swap engine selection: 0 = SM copy kernels (default), 1 = DMA copy engines
  * (cudaMemcpyAsync per chunk). Both are exact byte copies. */
 int ellm_set_swap_mode(ellm_pool* pool, int32_t mode);

@@ -149,6 +149,13 @@ struct Params {
   int32_t rec_dyn;           // record owner id of dynamic unit 0 (= G + n_vr)
   int32_t table_stride, n_vr, HG, G, T, L, layer, group, Hq;
   float scale_log2;
+  // a10 fused head gather (n_peer > 0; ellm_attention_gather): each merged output row is stored
+  // into EVERY rank's gather window over peer memory (NVLink P2P), at global q-head
+  // q_off + local head of a [n, Hq_out, D] layout, instead of into `out`; each CTA then adds the
+  // number of requests it merged to every rank's flag word (release, system scope).
+  __nv_bfloat16* gout[kMaxPeers];
+  uint32_t* gflag[kMaxPeers];
+  int32_t n_peer, Hq_out, q_off;
 };
 constexpr int kFirst = 1, kLast = 2, kDone = 4;  // stage metadata flags
 
@@ -224,7 +231,12 @@ __device__ __forceinline__ void merge_request(const Params& p, int vr, int rows,
       uint2 v;
       v.x = *reinterpret_cast<uint32_t*>(&lo);
       v.y = *reinterpret_cast<uint32_t*>(&hi);
-      *reinterpret_cast<uint2*>(p.out + (int64_t(ireq) * p.Hq + hg * HB * p.group + row) * D + 4 * e4) = v;
+      if (p.n_peer == 0) {
+        *reinterpret_cast<uint2*>(p.out + (int64_t(ireq) * p.Hq + hg * HB * p.group + row) * D + 4 * e4) = v;
+      } else {  // a10: the row goes to every rank's window (own window included)
+        const int64_t off = (int64_t(ireq) * p.Hq_out + p.q_off + hg * HB * p.group + row) * D + 4 * e4;
+        for (int i = 0; i < p.n_peer; ++i) *reinterpret_cast<uint2*>(p.gout[i] + off) = v;
+      }
     }
   }
 }
@@ -258,6 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ int4 s_meta[NST];          // per stage: {vr, tile within vr, record owner, flags | qslot}
   __shared__ int s_merge[kMaxMerges];   // requests this CTA completed last (merged at the end)
   __shared__ int s_n_merge;
+  __shared__ int s_n_now;               // requests warp 0 merged immediately (list was full)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * SB + kQSlots * QB);
   const uint32_t sbase = smem_u32(smem);
@@ -276,6 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(qempty0 + 8 * s, kConsumerWarps);
     }
     s_n_merge = 0;
+    s_n_now = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -633,13 +647,29 @@ __global__ void __launch_bounds__(kThreads, 1)
           else now = 1;        // deferred list full: warp 0 merges this one right away
         }
       }
-      if (__shfl_sync(0xffffffffu, now, 0)) merge_request<D, 1>(p, vr, rows, NSUB, HB, 0, 1);
+      if (__shfl_sync(0xffffffffu, now, 0)) {
+        merge_request<D, 1>(p, vr, rows, NSUB, HB, 0, 1);
+        if (lane == 0) ++s_n_now;
+      }
     }
   }
   // ---- end of this CTA's work: all consumer warps merge the requests it completed ----
   asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
   __threadfence();
   for (int k = 0; k < s_n_merge; ++k) merge_request<D, 8>(p, s_merge[k], rows, NSUB, HB, 0, kConsumerWarps);
+  if (p.n_peer > 0) {
+    // a10 signal: every thread's peer stores are made visible system-wide, the named barrier
+    // collects them, and thread 0 adds this CTA's merged-request count to every rank's flag with
+    // a system-scope release. A rank's flag reaches world * n_vr once all ranks' rows are in.
+    const int merged = s_n_merge + s_n_now;
+    __threadfence_system();
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+    if (threadIdx.x == 0 && merged > 0) {
+      __threadfence_system();
+      for (int i = 0; i < p.n_peer; ++i)
+        asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p.gflag[i]), "r"(merged) : "memory");
+    }
+  }
 }
 
 template <int D, int HB>
@@ -735,6 +765,13 @@ cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh,
   prm.group = sh.group;
   prm.Hq = sh.Hq;
   prm.scale_log2 = scale * 1.4426950408889634f;
+  prm.n_peer = plan.n_peer;
+  prm.Hq_out = plan.Hq_out;
+  prm.q_off = plan.q_off;
+  for (int i = 0; i < kMaxPeers; ++i) {
+    prm.gout[i] = static_cast<__nv_bfloat16*>(plan.gout[i]);
+    prm.gflag[i] = plan.gflag[i];
+  }
   cudaError_t e;
   if (sh.D == 128) {
     switch (sh.HB) {

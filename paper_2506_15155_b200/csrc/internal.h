@@ -86,6 +86,9 @@ struct TableUpdate {
 cudaError_t launch_table_scatter(int32_t* d_table, const TableUpdate* d_updates, int32_t n,
                                  cudaStream_t s);
 
+// a10: wait on `s` until *flag (this rank's gather flag word) >= target (wrapping compare).
+cudaError_t launch_gather_wait(const uint32_t* flag, uint32_t target, uint64_t timeout_ns, cudaStream_t s);
+
 struct AppendDesc {  // device-resident arrays, n entries (+1 for cum)
   const int32_t* req;
   const int32_t* pos0;
@@ -101,6 +104,8 @@ cudaError_t launch_kv_append(const AppendDesc& d, int32_t n, int64_t total_rows,
 cudaError_t launch_chunk_copy(uint8_t* dst_base, const int32_t* dst_idx, const uint8_t* src_base,
                               const int32_t* src_idx, int32_t n, int64_t chunk_bytes, int grid,
                               cudaStream_t s, int64_t seg_off = 0, int64_t seg_bytes = -1);
+
+constexpr int kMaxPeers = 8;            // ranks of a fused head gather (one 8-GPU box)
 
 struct AttnDesc {  // device-resident
   const int32_t* req;      // [n]
@@ -127,6 +132,11 @@ struct AttnPlan {
   const void* v_new = nullptr;
   uint8_t* pool = nullptr;
   int64_t chunk_bytes = 0;
+  // a10 fused head gather (ellm_attention_gather): per rank, where this call's rows and its
+  // merged-request count go; n_peer = 0 writes `out` as a local [n, Hq, D] tensor instead.
+  void* gout[kMaxPeers] = {};
+  uint32_t* gflag[kMaxPeers] = {};
+  int32_t n_peer = 0, Hq_out = 0, q_off = 0;
 };
 struct AttnShape {
   int32_t D, HB, HG, Hkv, Hq, group, T, L, TT, nsub;
@@ -268,6 +278,15 @@ struct ellm_pool {
 
   ellm::PrefillMaps pf_maps{};       // f4 tensor maps over the pool (encoded on first use)
   bool pf_ready = false;
+
+  // a10 fused head gather (ellm_gather_attach): every rank's gather window (flag words at +0,
+  // rows at +ELLM_GATHER_DATA_OFFSET), and per flag word the value this rank's own flag reaches
+  // once every rank has finished the calls issued so far
+  int32_t g_world = 0, g_rank = 0, g_hq_out = 0;
+  std::vector<uint8_t*> g_win;
+  int64_t g_win_bytes = 0;
+  std::vector<uint32_t> g_expect;
+  uint64_t g_timeout_ns = 20000000000ull;
 
   std::map<int32_t, std::pair<CUdeviceptr, size_t>> alias;
   int last_cuda_error = 0;

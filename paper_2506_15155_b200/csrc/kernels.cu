@@ -4,6 +4,7 @@
 //   chunk_copy      whole-chunk copies for deflate / inflate / migrate (a6-a8)
 // All three are HBM- (or host-link-) bound byte copies: 16-byte vector accesses, several
 // independent loads in flight per thread before the stores, grids sized to the SM count.
+#include <cstdio>
 #include "internal.h"
 
 namespace ellm {
@@ -129,6 +130,31 @@ cudaError_t launch_chunk_copy(uint8_t* dst_base, const int32_t* dst_idx, const u
   grid = int(std::max<int64_t>(1, std::min<int64_t>(grid, need)));
   chunk_copy_kernel<<<grid, 256, 0, s>>>(dst_base, dst_idx, src_base, src_idx, n, chunk_bytes, seg_off,
                                          seg_bytes);
+  return cudaGetLastError();
+}
+
+// a10 consumer side: one thread waits (acquire, system scope) until this rank's gather flag has
+// reached `target` — every rank's rows of the call are then in this rank's window. Bounded: after
+// timeout_ns it reports and traps, so a lost peer fails the stream loudly instead of hanging it.
+__global__ void gather_wait_kernel(const uint32_t* __restrict__ flag, uint32_t target, uint64_t timeout_ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (int32_t(v - target) >= 0) return;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) {
+      printf("ellm gather_wait: flag %u < target %u after %llu ns (peer rank missing?)\n", v, target,
+             static_cast<unsigned long long>(t - t0));
+      __trap();
+    }
+    __nanosleep(100);
+  }
+}
+
+cudaError_t launch_gather_wait(const uint32_t* flag, uint32_t target, uint64_t timeout_ns, cudaStream_t s) {
+  gather_wait_kernel<<<1, 1, 0, s>>>(flag, target, timeout_ns);
   return cudaGetLastError();
 }
 

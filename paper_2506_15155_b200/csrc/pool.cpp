@@ -647,7 +647,8 @@ int ellm_kv_append(ellm_pool* p, int32_t layer, int32_t n, const int32_t* reqs,
 
 // a4 + a5 — O4: exact softmax attention over the accumulated KV.
 static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t* reqs, const void* q,
-                          void* out, float scale, void* stream, const void* k_new, const void* v_new);
+                          void* out, float scale, void* stream, const void* k_new, const void* v_new,
+                          int64_t gather_off = -1);
 
 int ellm_paged_decode_attention(ellm_pool* p, int32_t layer, int32_t n, const int32_t* reqs,
                                 const void* q, void* out, float scale, void* stream) {
@@ -681,10 +682,123 @@ int ellm_decode_append_attention(ellm_pool* p, int32_t layer, int32_t n, const i
   return attention_impl(p, layer, n, reqs, q, out, scale, stream, k_new, v_new);
 }
 
+// ---- a10: head-sharded output gather fused into the attention epilogue over peer memory ----
+int ellm_gather_window_create(int32_t device, int64_t bytes, void** window_out, void* ipc_handle_out) {
+  if (!window_out || bytes <= ELLM_GATHER_DATA_OFFSET || device < 0) return ELLM_ERR_INVALID_ARG;
+  *window_out = nullptr;
+  cudaError_t e;
+  void* w = nullptr;
+  if ((e = cudaSetDevice(device)) != cudaSuccess || (e = cudaMalloc(&w, size_t(bytes))) != cudaSuccess)
+    return cuda_fail(nullptr, e);
+  if ((e = cudaMemset(w, 0, size_t(bytes))) != cudaSuccess ||
+      (ipc_handle_out && (e = cudaIpcGetMemHandle(static_cast<cudaIpcMemHandle_t*>(ipc_handle_out), w)) !=
+                             cudaSuccess) ||
+      (e = cudaDeviceSynchronize()) != cudaSuccess) {
+    cudaFree(w);
+    return cuda_fail(nullptr, e);
+  }
+  *window_out = w;
+  return ELLM_OK;
+}
+
+int ellm_gather_window_destroy(void* window) {
+  if (!window) return ELLM_ERR_INVALID_ARG;
+  return cudaFree(window) == cudaSuccess ? ELLM_OK : ELLM_ERR_CUDA;
+}
+
+int ellm_ipc_open(const void* ipc_handle, void** window_out) {
+  if (!ipc_handle || !window_out) return ELLM_ERR_INVALID_ARG;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, ipc_handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(window_out, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? ELLM_OK : cuda_fail(nullptr, e);
+}
+
+int ellm_ipc_close(void* window) {
+  if (!window) return ELLM_ERR_INVALID_ARG;
+  return cudaIpcCloseMemHandle(window) == cudaSuccess ? ELLM_OK : ELLM_ERR_CUDA;
+}
+
+int ellm_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (!dst || !src || bytes < 0) return ELLM_ERR_INVALID_ARG;
+  if (bytes == 0) return ELLM_OK;
+  return cudaMemcpyAsync(dst, src, size_t(bytes), cudaMemcpyDefault, S(stream)) == cudaSuccess ? ELLM_OK
+                                                                                                 : ELLM_ERR_CUDA;
+}
+
+int ellm_gather_attach(ellm_pool* p, int32_t world, int32_t rank, int32_t heads_q_total,
+                       void* const* windows, int64_t window_bytes) {
+  if (!p || !windows) return ELLM_ERR_INVALID_ARG;
+  if (world < 1 || world > ellm::kMaxPeers || rank < 0 || rank >= world) return ELLM_ERR_OUT_OF_RANGE;
+  if (heads_q_total != world * p->cfg.n_heads_q || window_bytes <= ELLM_GATHER_DATA_OFFSET ||
+      p->cfg.n_layers > ELLM_GATHER_DATA_OFFSET / 4)
+    return ELLM_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < world; ++i)
+    if (!windows[i] || reinterpret_cast<uintptr_t>(windows[i]) % 256) return ELLM_ERR_INVALID_ARG;
+  if (!p->has_dev) return ELLM_ERR_NO_DEVICE;
+  // this rank's flags as they stand (zero for a fresh window): all ranks must be idle here
+  std::vector<uint32_t> cur(size_t(p->cfg.n_layers));
+  cudaError_t e = cudaMemcpy(cur.data(), windows[rank], cur.size() * 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(p, e);
+  p->g_world = world;
+  p->g_rank = rank;
+  p->g_hq_out = heads_q_total;
+  p->g_win.assign(reinterpret_cast<uint8_t* const*>(windows), reinterpret_cast<uint8_t* const*>(windows) + world);
+  p->g_win_bytes = window_bytes;
+  p->g_expect = cur;
+  if (const char* t = std::getenv("ELLM_GATHER_TIMEOUT_MS")) p->g_timeout_ns = uint64_t(std::atoll(t)) * 1000000ull;
+  return ELLM_OK;
+}
+
+int ellm_gather_detach(ellm_pool* p) {
+  if (!p) return ELLM_ERR_INVALID_ARG;
+  p->g_world = 0;
+  p->g_win.clear();
+  p->g_expect.clear();
+  return ELLM_OK;
+}
+
+int ellm_attention_gather(ellm_pool* p, int32_t layer, int32_t n, const int32_t* reqs, const void* k_new,
+                          const void* v_new, const void* q, int64_t out_offset, float scale, void* stream) {
+  if (!p || n < 0 || (n > 0 && !reqs)) return ELLM_ERR_INVALID_ARG;
+  if (layer < 0 || layer >= p->cfg.n_layers) return ELLM_ERR_OUT_OF_RANGE;
+  if (!check_reqs_range(p, n, reqs)) return ELLM_ERR_OUT_OF_RANGE;
+  if (p->g_world == 0 || out_offset < 0 || out_offset % 16) return ELLM_ERR_INVALID_ARG;
+  const int64_t rows_bytes = int64_t(n) * p->g_hq_out * p->cfg.head_dim * 2;
+  if (out_offset + rows_bytes > p->g_win_bytes - ELLM_GATHER_DATA_OFFSET) return ELLM_ERR_OUT_OF_RANGE;
+  if (k_new || v_new) {  // fused decode append: as ellm_decode_append_attention
+    if (has_dup(n, reqs) || !k_new || !v_new) return ELLM_ERR_INVALID_ARG;
+    for (int32_t i = 0; i < n; ++i)
+      if (p->pending[size_t(reqs[i])] != 1) return ELLM_ERR_INVALID_ARG;
+  } else {
+    for (int32_t i = 0; i < n; ++i)
+      if (p->len[size_t(reqs[i])] == 0) return ELLM_ERR_INVALID_ARG;
+  }
+  for (int32_t i = 0; i < n; ++i)
+    if (p->nonres[size_t(reqs[i])] > 0) return ELLM_ERR_NOT_RESIDENT;
+  if (!p->has_dev) return ELLM_ERR_NO_DEVICE;
+  if (n == 0) return ELLM_OK;
+  return attention_impl(p, layer, n, reqs, q, p->g_win[size_t(p->g_rank)] + ELLM_GATHER_DATA_OFFSET + out_offset,
+                        scale, stream, k_new, v_new, out_offset);
+}
+
+int ellm_gather_wait(ellm_pool* p, int32_t layer, void* stream) {
+  if (!p) return ELLM_ERR_INVALID_ARG;
+  if (layer < 0 || layer >= p->cfg.n_layers) return ELLM_ERR_OUT_OF_RANGE;
+  if (p->g_world == 0) return ELLM_ERR_INVALID_ARG;
+  if (!p->has_dev) return ELLM_ERR_NO_DEVICE;
+  const uint32_t* flag = reinterpret_cast<const uint32_t*>(p->g_win[size_t(p->g_rank)]) + layer;
+  cudaError_t e = launch_gather_wait(flag, p->g_expect[size_t(layer)], p->g_timeout_ns, S(stream));
+  if (e != cudaSuccess) return cuda_fail(p, e);
+  ++p->launches;
+  return ELLM_OK;
+}
+
 }  // extern "C"
 
 static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t* reqs, const void* q,
-                          void* out, float scale, void* stream, const void* k_new, const void* v_new) {
+                          void* out, float scale, void* stream, const void* k_new, const void* v_new,
+                          int64_t gather_off) {
   if (!q || !out || !std::isfinite(scale)) return ELLM_ERR_INVALID_ARG;
   const AttnShape& a = p->ash;
   const int32_t n_vr = n * a.HG;
@@ -815,6 +929,15 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
   plan.v_new = v_new;
   plan.pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
   plan.chunk_bytes = p->chunk_bytes;
+  if (gather_off >= 0) {  // a10: rows to every rank's window, merged counts to every rank's flag
+    plan.n_peer = p->g_world;
+    plan.Hq_out = p->g_hq_out;
+    plan.q_off = p->g_rank * a.Hq;
+    for (int32_t i = 0; i < p->g_world; ++i) {
+      plan.gout[i] = p->g_win[size_t(i)] + ELLM_GATHER_DATA_OFFSET + gather_off;
+      plan.gflag[i] = reinterpret_cast<uint32_t*>(p->g_win[size_t(i)]) + layer;
+    }
+  }
   int launches = 0;
   cudaError_t e = launch_paged_attention(p->tmap, a, ad, n, n_vr, plan, p->d_table,
                                          p->cfg.max_chunks_per_request, layer, q, out, p->d_part,
@@ -823,6 +946,8 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
   if (e != cudaSuccess) return cuda_fail(p, e);
   // tickets consumed: every unit once, plus the two outstanding tickets each CTA ends with
   if (plan.n_dyn > 0) p->ticket_base += uint64_t(plan.n_dyn) + 2 * uint64_t(plan.G);
+  // every rank merges its n_vr requests once and adds them to every rank's flag word
+  if (gather_off >= 0) p->g_expect[size_t(layer)] += uint32_t(p->g_world) * uint32_t(n_vr);
   return p->ring.commit(S(stream));
 }
 

@@ -91,6 +91,15 @@ _SIGS = {
     "ellm_read_host_slot": (ctypes.c_int, [_P, _I64, _V]),
     "ellm_alias_request": (ctypes.c_int, [_P, _I32, ctypes.POINTER(_V)]),
     "ellm_unalias_request": (ctypes.c_int, [_P, _I32]),
+    "ellm_gather_window_create": (ctypes.c_int, [_I32, _I64, ctypes.POINTER(_V), _P]),
+    "ellm_gather_window_destroy": (ctypes.c_int, [_V]),
+    "ellm_ipc_open": (ctypes.c_int, [_P, ctypes.POINTER(_V)]),
+    "ellm_ipc_close": (ctypes.c_int, [_V]),
+    "ellm_gather_attach": (ctypes.c_int, [_P, _I32, _I32, _I32, _P, _I64]),
+    "ellm_gather_detach": (ctypes.c_int, [_P]),
+    "ellm_attention_gather": (ctypes.c_int, [_P, _I32, _I32, _P, _V, _V, _V, _I64, ctypes.c_float, _V]),
+    "ellm_gather_wait": (ctypes.c_int, [_P, _I32, _V]),
+    "ellm_memcpy_async": (ctypes.c_int, [_V, _V, _I64, _V]),
     "ellm_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "ellm_last_cuda_error": (ctypes.c_int, [_P]),
     "ellm_kernel_launches": (_I64, [_P]),
@@ -190,6 +199,28 @@ class Pool:
         r = _i32(reqs)
         return ellm_decode_append_attention(self._h, layer, len(r), _ptr(r), _dptr(k_new), _dptr(v_new),
                                             _dptr(q), _dptr(out), float(scale), _sptr(stream))
+
+    # ---- a10: head-sharded output gather fused into the attention epilogue (peer memory) ----
+    def gather_attach(self, world: int, rank: int, heads_q_total: int, windows, window_bytes: int) -> int:
+        """windows[i]: device address of rank i's gather window in this process."""
+        arr = (_V * len(windows))(*[int(w) for w in windows])
+        return ellm_gather_attach(self._h, int(world), int(rank), int(heads_q_total), ctypes.cast(arr, _P),
+                                  int(window_bytes))
+
+    def gather_detach(self) -> int:
+        return ellm_gather_detach(self._h)
+
+    def attention_gather(self, layer, reqs, q, out_offset, scale, k_new=None, v_new=None, stream=None) -> int:
+        """Attention (fused with the decode append when k_new / v_new are given) whose
+        [n, Hq_total, d] output rows land in every rank's window at out_offset."""
+        r = _i32(reqs)
+        return ellm_attention_gather(self._h, int(layer), len(r), _ptr(r),
+                                     _dptr(k_new) if k_new is not None else None,
+                                     _dptr(v_new) if v_new is not None else None, _dptr(q), int(out_offset),
+                                     float(scale), _sptr(stream))
+
+    def gather_wait(self, layer, stream=None) -> int:
+        return ellm_gather_wait(self._h, int(layer), _sptr(stream))
 
     def release(self, req, stream=None) -> int:
         return ellm_release(self._h, int(req), _sptr(stream))
@@ -333,3 +364,39 @@ def vmm_granularity(device: int = 0) -> int:
     if rc != OK:
         raise EllmError(rc, "ellm_vmm_granularity")
     return g.value
+
+
+GATHER_DATA_OFFSET = 4096  # include/ellm.h ELLM_GATHER_DATA_OFFSET
+IPC_HANDLE_BYTES = 64
+
+
+def gather_window_create(device: int, nbytes: int) -> tuple[int, bytes]:
+    """(device address, 64-byte cudaIpcMemHandle) of a fresh zeroed gather window."""
+    w = _V()
+    h = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+    rc = ellm_gather_window_create(int(device), int(nbytes), ctypes.byref(w), ctypes.cast(h, _P))
+    if rc != OK:
+        raise EllmError(rc, "ellm_gather_window_create")
+    return w.value, h.raw
+
+
+def gather_window_destroy(addr: int) -> int:
+    return ellm_gather_window_destroy(addr)
+
+
+def ipc_open(handle: bytes) -> int:
+    w = _V()
+    buf = ctypes.create_string_buffer(bytes(handle), IPC_HANDLE_BYTES)
+    rc = ellm_ipc_open(ctypes.cast(buf, _P), ctypes.byref(w))
+    if rc != OK:
+        raise EllmError(rc, "ellm_ipc_open")
+    return w.value
+
+
+def ipc_close(addr: int) -> int:
+    return ellm_ipc_close(addr)
+
+
+def memcpy_async(dst, src, nbytes: int, stream=None) -> int:
+    """cudaMemcpyAsync(cudaMemcpyDefault) between raw addresses / tensors (window readback)."""
+    return ellm_memcpy_async(_dptr(dst), _dptr(src), int(nbytes), _sptr(stream))

@@ -40,3 +40,78 @@ def gather_heads(out_local, world: int, group=None, out=None):
         out.copy_(full)
         return out
     return full
+
+
+def gather_window_bytes(n_layers: int, batch: int, heads_q_total: int, head_dim: int) -> int:
+    """Window size for one [B, Hq_total, d] bf16 output slot per layer (plus the flag words)."""
+    from paper_2506_15155_b200.ellm import GATHER_DATA_OFFSET
+    return GATHER_DATA_OFFSET + n_layers * layer_stride(batch, heads_q_total, head_dim)
+
+
+def layer_stride(batch: int, heads_q_total: int, head_dim: int) -> int:
+    """Bytes of one layer's gathered output [B, Hq_total, d] bf16 (16-B aligned)."""
+    return (batch * heads_q_total * head_dim * 2 + 15) // 16 * 16
+
+
+def exchange_handles(handle: bytes, world: int, group=None) -> list[bytes]:
+    """All ranks' 64-byte IPC handles, rank order (torch.distributed object all-gather; works
+    on gloo and nccl)."""
+    import torch.distributed as dist
+    if world == 1:
+        return [bytes(handle)]
+    out = [None] * world
+    dist.all_gather_object(out, bytes(handle), group=group)
+    return [bytes(h) for h in out]
+
+
+class PeerGather:
+    """a10 fused head gather over peer memory (include/ellm.h).
+
+    Each rank allocates one gather window, the IPC handles are exchanged over the process
+    group, every rank maps the others' windows (cudaIpcOpenMemHandle: NVLink P2P between the
+    GPUs of one box) and attaches all N to its pool. From then on
+    ``pool.attention_gather(l, ..., out_offset=self.offset(l))`` writes each finished output row
+    straight into every rank's window and ``pool.gather_wait(l)`` orders the consumer after all
+    ranks' rows — no separate collective launch. ``out(l)`` is the device address of layer l's
+    gathered [B, Hq_total, d] rows in this rank's own window."""
+
+    def __init__(self, pool, world: int, rank: int, heads_q_total: int, n_layers: int, batch: int,
+                 head_dim: int, device: int, group=None):
+        from paper_2506_15155_b200 import ellm
+        self.ellm = ellm
+        self.pool, self.world, self.rank = pool, world, rank
+        self.stride = layer_stride(batch, heads_q_total, head_dim)
+        self.nbytes = gather_window_bytes(n_layers, batch, heads_q_total, head_dim)
+        self.own, handle = ellm.gather_window_create(device, self.nbytes)
+        self.opened = []
+        handles = exchange_handles(handle, world, group)
+        windows = []
+        for i, h in enumerate(handles):
+            if i == rank:
+                windows.append(self.own)
+            else:
+                a = ellm.ipc_open(h)
+                self.opened.append(a)
+                windows.append(a)
+        self.windows = windows
+        rc = pool.gather_attach(world, rank, heads_q_total, windows, self.nbytes)
+        if rc != ellm.OK:
+            self.close()
+            raise ellm.EllmError(rc, "ellm_gather_attach")
+
+    def offset(self, layer: int) -> int:
+        return layer * self.stride
+
+    def out(self, layer: int) -> int:
+        return self.own + self.ellm.GATHER_DATA_OFFSET + self.offset(layer)
+
+    def close(self):
+        if self.pool is not None:
+            self.pool.gather_detach()
+        for a in self.opened:
+            self.ellm.ipc_close(a)
+        self.opened = []
+        if self.own:
+            self.ellm.gather_window_destroy(self.own)
+            self.own = 0
+        self.pool = None

@@ -48,7 +48,10 @@ def _worker(rank, world, port, q):
         # gather of head-sharded outputs
         ref = torch.arange(4 * Hq * d, dtype=torch.float32).reshape(4, Hq, d)
         full = shard.gather_heads(ref[:, q0:q1].contiguous(), world)
-        q.put((rank, same_tables, bool(torch.equal(full, ref)), (kv0, kv1, q0, q1)))
+        # a10 setup: IPC handles of every rank's gather window, exchanged in rank order
+        hs = shard.exchange_handles(bytes([rank + 1]) * 64, world)
+        ok_handles = hs == [bytes([i + 1]) * 64 for i in range(world)]
+        q.put((rank, same_tables, bool(torch.equal(full, ref)), (kv0, kv1, q0, q1), ok_handles))
     finally:
         dist.destroy_process_group()
 
@@ -69,9 +72,31 @@ def test_two_rank_sharding_gloo():
     assert all(r[1] for r in res), "chunk tables differ between shards"
     assert all(r[2] for r in res), "head gather mismatch"
     assert res[0][3] == (0, 4, 0, 16) and res[1][3] == (4, 8, 16, 32)
+    assert all(r[4] for r in res), "IPC handle exchange out of rank order"
 
 
 def test_partition_errors():
     with pytest.raises(ValueError):
         shard.head_partition(32, 8, 3, 0)
     assert [shard.head_partition(64, 8, 8, r)[2:] for r in (0, 7)] == [(0, 8), (56, 64)]
+
+
+def test_gather_attach_validation_host_only():
+    """a10 (include/ellm.h gather_attach / attention_gather / gather_wait): argument checks run
+    before any device work; a host-only pool then reports NO_DEVICE."""
+    from paper_2506_15155_b200 import ellm
+    L, Hq_loc, Hkv_loc, d, B = 2, 16, 4, 128, 4
+    pool = ellm.Pool(ellm.DEVICE_NONE, L, Hq_loc, Hkv_loc, d, 32, 64, 64, B, 16, 0)
+    nbytes = shard.gather_window_bytes(L, B, 2 * Hq_loc, d)
+    assert nbytes == 4096 + L * B * 32 * d * 2
+    wins = [1 << 20, 2 << 20]
+    assert pool.attention_gather(0, [0], 0, 0, 1.0) == ellm.INVALID_ARG   # not attached
+    assert pool.gather_wait(0) == ellm.INVALID_ARG
+    assert pool.gather_attach(0, 0, Hq_loc, wins, nbytes) == ellm.OUT_OF_RANGE
+    assert pool.gather_attach(9, 0, 9 * Hq_loc, wins * 5, nbytes) == ellm.OUT_OF_RANGE
+    assert pool.gather_attach(2, 2, 2 * Hq_loc, wins, nbytes) == ellm.OUT_OF_RANGE
+    assert pool.gather_attach(2, 1, 3 * Hq_loc, wins, nbytes) == ellm.INVALID_ARG   # heads
+    assert pool.gather_attach(2, 1, 2 * Hq_loc, [1 << 20, 17], nbytes) == ellm.INVALID_ARG  # align
+    assert pool.gather_attach(2, 1, 2 * Hq_loc, wins, 4096) == ellm.INVALID_ARG
+    assert pool.gather_attach(2, 1, 2 * Hq_loc, wins, nbytes) == ellm.NO_DEVICE
+    assert shard.layer_stride(3, 5, 64) == 1920 and shard.layer_stride(1, 1, 4) == 16
