@@ -35,10 +35,18 @@ FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback (only
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--steps", type=int, default=None, help="timed steps (default 40; c3: 4 swap rounds)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ellm", "reference"], default="ellm")
-    ap.add_argument("--workload", choices=["c2", "c4"], default="c2")
+    ap.add_argument("--workload", choices=["c2", "c3", "c4"], default="c2",
+                    help="c2 (default): 8B 32x32K; c3: 8B-262K 16x128K under memory pressure; c4: 70B 64x8K")
+    ap.add_argument("--swap-every", type=int, default=48,
+                    help="c3: decode steps per offload/fetch round")
+    ap.add_argument("--swap-mode", choices=["sm", "ce", "mixed"], default="ce",
+                    help="c3: swap with the SM copy kernels, the DMA copy engines, or copy engines for "
+                         "swap-out and SM kernels for swap-in (mixed)")
+    ap.add_argument("--resident", type=int, default=0,
+                    help="c3: requests decoding in HBM (0 = as many as fit beside one in flight)")
     ap.add_argument("--gather", choices=["p2p", "nccl"], default="p2p",
                     help="N>1 head gather: fused into the attention epilogue over peer memory (p2p) "
                          "or a separate NCCL all-gather per layer")
@@ -49,7 +57,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true",
                     help="wrap the timed steps in cudaProfilerStart/Stop (ncu --profile-from-start off)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.steps is None:
+        a.steps = 4 * a.swap_every if a.workload == "c3" else 40
+    return a
 
 
 def hbm_peak():
@@ -168,7 +179,7 @@ def run_reference(args):
         return
     from inputs import workload as W
     import oracle
-    wl = W.c2() if args.workload == "c2" else W.c4()
+    wl = {"c2": W.c2, "c3": W.c3, "c4": W.c4}[args.workload]()
     k, v = W.host_kv(wl, 0, 0, wl.context)
     q = W.host_q(wl, 0, 0)
     scale = 1.0 / (wl.head_dim ** 0.5)
@@ -212,6 +223,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "c3":
+        return run_c3(args)
     import numpy as np
     import torch
     from paper_2506_15155_b200 import ellm
@@ -568,6 +581,217 @@ def main():
     pool.close()
     if dist:
         dist.destroy_process_group()
+
+
+def run_c3(args):
+    """BASELINE.json configs[2]: LLaMA-3-8B-262K shape, batch 16 x 128K context, decode under
+    memory pressure. 256 GiB of KV does not fit one B200, so the pool holds R + 1 requests'
+    chunks: R decode (the resident set) and one region is in flight. Every `swap_every` steps
+    the least recently admitted request of the set is offloaded (deflate) and the next
+    host-resident request is fetched into the freed chunks (inflate), on a second stream
+    so the swap overlaps the decode of the set; the fetched request joins the set
+    at the next round. All 16 requests progress round-robin; value = tokens/s of the whole job
+    (R per step) over exactly K timed steps, swaps included."""
+    import numpy as np
+    import torch
+    from paper_2506_15155_b200 import ellm
+    from inputs import workload as W
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        if int(os.environ.get("RANK", "0")) == 0:
+            print(json.dumps({"metric": METRIC, "unavailable": "c3 is a single-GPU configuration"}), flush=True)
+        return
+    torch.cuda.set_device(0)
+    wl = W.c3()
+    total, L, Hq, Hkv, d, T = wl.batch, wl.n_layers, wl.hq_local, wl.hkv_local, wl.head_dim, wl.tokens_per_chunk
+    cpr = wl.chunks_per_request
+    req_bytes = cpr * wl.chunk_bytes()
+    free, _ = torch.cuda.mem_get_info()
+    fit = min(total, int((free - (5 << 30)) // req_bytes)) - 1
+    R = min(fit, args.resident) if args.resident else fit  # measured best (DESIGN.md §5, C3)
+    if R < 1:
+        raise SystemExit("c3: not enough free HBM for one resident request plus one in flight")
+    regions = R + 1
+    host_reqs = total - R
+    avail = 0
+    for ln in open("/proc/meminfo"):
+        if ln.startswith("MemAvailable"):
+            avail = int(ln.split()[1]) * 1024
+    if host_reqs * req_bytes > avail - (24 << 30):
+        raise SystemExit(f"c3 needs {host_reqs * req_bytes >> 30} GiB of pinned host memory, "
+                         f"{avail >> 30} GiB available")
+    t0 = time.perf_counter()
+    pool = ellm.Pool(0, L, Hq, Hkv, d, T, regions * cpr, regions * cpr, total, cpr, host_reqs * cpr)
+    t_create = time.perf_counter() - t0
+    cs = torch.cuda.current_stream()
+    sp = cs.cuda_stream
+    out_mode = 0 if args.swap_mode == "sm" else 1
+    in_mode = 1 if args.swap_mode == "ce" else 0
+    pool.set_swap_mode(out_mode)
+    # placement: requests R+1.. are prefilled through the pool and offloaded; 0..R stay
+    host_q = []
+    for r in range(R + 1, total):
+        W.fill_request(pool, wl, r, wl.context)
+        rc, slots = pool.deflate(pool.table(r)[0].tolist(), sp)
+        if rc:
+            raise ellm.EllmError(rc, "c3 offload")
+        host_q.append((r, slots))
+    for r in range(R + 1):
+        W.fill_request(pool, wl, r, wl.context)
+    torch.cuda.synchronize()
+    D = list(range(R))            # the decoding set, oldest first
+    incoming, in_ev = R, None     # fetched request, joins D at the next round
+    sw = torch.cuda.Stream()
+    scale = 1.0 / (d ** 0.5)
+    ones = [1] * R
+    slot_wl = W.Workload(**{**wl.__dict__, "batch": R})
+    NIN = 8  # input ring: Q / new K,V of the R decode slots for 8 steps (synthetic values)
+    inputs = [W.decode_inputs(slot_wl, s, np.full(R, wl.context + s, np.int64)) for s in range(NIN)]
+    out = torch.empty((L, R, Hq, d), dtype=torch.bfloat16, device="cuda")
+    attn_ev, swap_ev, swap_bytes = [], [], []
+    tokens = {r: 0 for r in range(total)}
+
+    def transition():
+        nonlocal incoming, in_ev
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        sw.wait_event(ev)                      # X's last attention reads are done
+        x = D.pop(0)
+        if in_ev is not None:
+            cs.wait_event(in_ev)               # the fetched request's bytes have landed
+        D.append(incoming)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(sw)
+        ids = pool.table(x)[0].tolist()
+        pool.set_swap_mode(out_mode)
+        rc, slots = pool.deflate(ids, sw.cuda_stream)
+        if rc:
+            raise ellm.EllmError(rc, "c3 deflate")
+        host_q.append((x, slots))
+        y, yslots = host_q.pop(0)
+        pool.set_swap_mode(in_mode)
+        rc, _ = pool.inflate(yslots, sw.cuda_stream)
+        if rc:
+            raise ellm.EllmError(rc, "c3 inflate")
+        e1.record(sw)
+        in_ev, incoming = e1, y
+        swap_ev.append((e0, e1))
+        swap_bytes.append((len(ids) + len(yslots)) * pool.chunk_bytes)
+
+    def step(s, record=False, host=None):
+        if s and s % args.swap_every == 0:
+            transition()
+        q, k, v = inputs[s % NIN] if host is None else host
+        rc = pool.reserve(D, ones, sp)
+        if rc:
+            raise ellm.EllmError(rc, "c3 reserve")
+        for r in D:
+            tokens[r] += 1
+        lens_now = [int(pool.table(r)[1]) for r in D] if record else None
+        for l in range(L):
+            if record:
+                a0 = torch.cuda.Event(enable_timing=True)
+                a0.record(cs)
+            rc = pool.decode_append_attention(l, D, k[l], v[l], q[l], out[l], scale, sp)
+            if rc:
+                raise ellm.EllmError(rc, "c3 decode_append_attention")
+            if record:
+                a1 = torch.cuda.Event(enable_timing=True)
+                a1.record(cs)
+                attn_ev.append((a0, a1, lens_now))
+
+    s_glob = 0
+    for _ in range(args.warmup):
+        step(s_glob)
+        s_glob += 1
+    torch.cuda.synchronize()
+    launches0 = pool.kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_swaps0 = len(swap_ev)
+    with ClockSampler(gpu_id_for(0)) as clk:
+        clk.wait_first_sample()
+        ev0.record(cs)
+        for _ in range(args.steps):
+            step(s_glob, record=True)
+            s_glob += 1
+        ev1.record(cs)
+        torch.cuda.synchronize()
+    launches = pool.kernel_launches() - launches0
+    el_ms = ev0.elapsed_time(ev1)
+    value = R * args.steps / (el_ms / 1e3)
+    timed_swaps = swap_ev[n_swaps0:]
+    swap_ms = [a.elapsed_time(b) for a, b in timed_swaps]
+    swap_gbs = [nb / (ms / 1e3) / 1e9 for nb, ms in zip(swap_bytes[n_swaps0:], swap_ms)]
+    attn_ms = [a.elapsed_time(b) for a, b, _ in attn_ev]
+    alg = [sum(lens) * Hkv * d * 4 + 2 * R * Hq * d * 2 + 4 * sum((n + T - 1) // T for n in lens)
+           for _, _, lens in attn_ev]
+    attn_mean = statistics.mean(attn_ms)
+    achieved = statistics.mean(alg) / (attn_mean / 1e3) / 1e9
+    peak, peak_src = hbm_peak()
+
+    # the same resident set without swapping (isolated decode), and end to end through host buffers
+    torch.cuda.synchronize()
+    if in_ev is not None:
+        in_ev.synchronize()
+    i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_iso = min(args.swap_every - 1, 16)
+    s_iso = (s_glob // args.swap_every) * args.swap_every + 1  # no transition inside
+    i0.record(cs)
+    for j in range(n_iso):
+        step(s_iso + j)
+    i1.record(cs)
+    torch.cuda.synchronize()
+    iso_ms = i0.elapsed_time(i1) / n_iso
+    e2e = None
+    if not args.no_e2e:
+        n_e2e = args.swap_every  # one full round, its transition included
+        hin = [tuple(x.cpu().pin_memory() for x in inputs[j % NIN]) for j in range(n_e2e)]
+        dev = tuple(torch.empty_like(x) for x in inputs[0])
+        hout = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        s_e = ((s_glob + n_iso) // args.swap_every + 1) * args.swap_every
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cs)
+        for j in range(n_e2e):
+            for dt, ht in zip(dev, hin[j]):
+                dt.copy_(ht, non_blocking=True)
+            step(s_e + j, host=dev)
+            hout.copy_(out, non_blocking=True)
+        e1.record(cs)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        e2e = {"value": round(R * n_e2e / (ems / 1e3), 3), "unit": UNIT,
+               "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() for x in hin[0])),
+               "d2h_bytes_per_step": int(hout.numel() * hout.element_size()),
+               "ms_per_step": round(ems / n_e2e, 3), "steps": n_e2e}
+    torch.cuda.synchronize()
+    cpu = None
+    if not args.no_cpu_baseline:
+        per_rl, reps, threads = oracle_sample(wl)
+        cpu = cpu_baseline_obj(wl, per_rl, reps, threads)
+    line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(el_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded counter-based generator, 3 needles per request/layer/kv-head)",
+            "config": {**workload_config(wl, 1), "resident_requests": R, "host_requests": total - R - 1,
+                       "in_flight_requests": 1, "swap_every_steps": args.swap_every,
+                       "swap_mode": args.swap_mode, "pool_gib": round(regions * req_bytes / 2 ** 30, 1),
+                       "host_slots_gib": round(host_reqs * req_bytes / 2 ** 30, 1)},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "kernel": "paged_attn_kernel (ellm_decode_append_attention, one launch per layer)",
+                         "alg_bytes_per_launch": int(statistics.mean(alg)), "launch_ms": round(attn_mean, 4),
+                         "peak_source": peak_src},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+            "c3": {"isolated_decode_ms_per_step": round(iso_ms, 4),
+                   "swap_overhead_frac": round(1 - iso_ms / (el_ms / args.steps), 4),
+                   "swaps_timed": len(timed_swaps),
+                   "swap_round_ms": [round(x, 1) for x in swap_ms],
+                   "swap_gbs_bidir_serial": [round(x, 2) for x in swap_gbs],
+                   "bytes_per_swap_round": swap_bytes[-1] if swap_bytes else 0,
+                   "tokens_per_request": [tokens[r] for r in range(total)],
+                   "pool_create_s": round(t_create, 2)}}
+    print(json.dumps(line), flush=True)
+    pool.close()
 
 
 def measure_swap(pool, wl, stream):

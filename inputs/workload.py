@@ -97,6 +97,13 @@ def c4(world=1, rank=0, batch=64) -> Workload:
                     tokens_per_chunk=32 * world, world=world, rank=rank)
 
 
+def c3(batch=16) -> Workload:
+    """BASELINE.json configs[2]: LLaMA-3-8B-262K shape, batch 16 x 128K context (seed 2): 256 GiB
+    of KV in 2 MiB chunks, more than one B200 holds, so part of the batch lives in host slots."""
+    return Workload("c3-llama3-8b-262k-16x128k", 32, 32, 8, 128, batch, 131072, seed=2,
+                    tokens_per_chunk=16, decode_headroom=512)
+
+
 def c1() -> Workload:
     return Workload("c1-tiny", 1, 4, 2, 64, 4, 300, seed=0, tokens_per_chunk=16, decode_headroom=64)
 

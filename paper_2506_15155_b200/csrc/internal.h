@@ -101,9 +101,14 @@ cudaError_t launch_kv_append(const AppendDesc& d, int32_t n, int64_t total_rows,
 
 // Chunk copy: dst_base + dst_idx[i]*bytes <- src_base + src_idx[i]*bytes, i < n.
 // (seg_off, seg_bytes): copy only that byte range of each chunk (seg_bytes < 0: whole chunk).
+// `work`: a device word that is 0 when the kernel starts, the work-claim counter (callers upload
+// it with the index lists, so every call has its own).
 cudaError_t launch_chunk_copy(uint8_t* dst_base, const int32_t* dst_idx, const uint8_t* src_base,
                               const int32_t* src_idx, int32_t n, int64_t chunk_bytes, int grid,
-                              cudaStream_t s, int64_t seg_off = 0, int64_t seg_bytes = -1);
+                              uint32_t* work, cudaStream_t s, int64_t seg_off = 0, int64_t seg_bytes = -1);
+inline uint32_t* work_word(const int32_t* uploaded, int64_t index) {
+  return reinterpret_cast<uint32_t*>(const_cast<int32_t*>(uploaded + index));
+}
 
 constexpr int kMaxPeers = 8;            // ranks of a fused head gather (one 8-GPU box)
 

@@ -71,26 +71,39 @@ __global__ void __launch_bounds__(256) kv_append_kernel(
 // iteration with 8 x 16 B loads in flight per lane before its stores (latency hiding for HBM
 // and for host memory over PCIe).
 constexpr int kCopyUnit = 4096;
+constexpr int kCopyGrab = 16;  // units (64 KiB) a warp claims per atomic
 __global__ void __launch_bounds__(256) chunk_copy_kernel(uint8_t* __restrict__ dst_base,
                                                          const int32_t* __restrict__ dst_idx,
                                                          const uint8_t* __restrict__ src_base,
                                                          const int32_t* __restrict__ src_idx,
                                                          int32_t n, int64_t chunk_bytes, int64_t seg_off,
-                                                         int64_t seg_bytes) {
+                                                         int64_t seg_bytes, uint32_t* __restrict__ work) {
+  // Work is claimed dynamically (one atomic per 64 KiB) rather than by a static grid stride: a
+  // swap usually runs beside the persistent attention kernel, which leaves room for one copy
+  // CTA per SM, so with a static split the CTAs that only become resident after the first
+  // wave did their share serially at the end (measured beside C2 decode: 30 GB/s static vs
+  // 52 GB/s claimed, the isolated rate).
   const int lane = threadIdx.x & 31;
   const int64_t units_per_chunk = seg_bytes / kCopyUnit;
   const int64_t total = int64_t(n) * units_per_chunk;
-  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t w = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total; w += warps) {
-    const int64_t i = w / units_per_chunk;
-    const int64_t off = seg_off + (w % units_per_chunk) * kCopyUnit;
-    const uint4* s = reinterpret_cast<const uint4*>(src_base + int64_t(__ldg(src_idx + i)) * chunk_bytes + off);
-    uint4* d = reinterpret_cast<uint4*>(dst_base + int64_t(__ldg(dst_idx + i)) * chunk_bytes + off);
-    uint4 v[8];
+  for (;;) {
+    uint32_t g = 0;
+    if (lane == 0) g = atomicAdd(work, 1u);
+    g = __shfl_sync(0xffffffffu, g, 0);
+    const int64_t u0 = int64_t(g) * kCopyGrab;
+    if (u0 >= total) break;
+    const int64_t u1 = u0 + kCopyGrab < total ? u0 + kCopyGrab : total;
+    for (int64_t w = u0; w < u1; ++w) {
+      const int64_t i = w / units_per_chunk;
+      const int64_t off = seg_off + (w % units_per_chunk) * kCopyUnit;
+      const uint4* s = reinterpret_cast<const uint4*>(src_base + int64_t(__ldg(src_idx + i)) * chunk_bytes + off);
+      uint4* d = reinterpret_cast<uint4*>(dst_base + int64_t(__ldg(dst_idx + i)) * chunk_bytes + off);
+      uint4 v[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = __ldcs(s + k * 32 + lane);
+      for (int k = 0; k < 8; ++k) v[k] = __ldcs(s + k * 32 + lane);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) __stcs(d + k * 32 + lane, v[k]);
+      for (int k = 0; k < 8; ++k) __stcs(d + k * 32 + lane, v[k]);
+    }
   }
 }
 
@@ -120,16 +133,17 @@ cudaError_t launch_kv_append(const AppendDesc& d, int32_t n, int64_t total_rows,
 
 cudaError_t launch_chunk_copy(uint8_t* dst_base, const int32_t* dst_idx, const uint8_t* src_base,
                               const int32_t* src_idx, int32_t n, int64_t chunk_bytes, int grid,
-                              cudaStream_t s, int64_t seg_off, int64_t seg_bytes) {
+                              uint32_t* work, cudaStream_t s, int64_t seg_off, int64_t seg_bytes) {
   if (n <= 0) return cudaSuccess;
+  if (work == nullptr) return cudaErrorInvalidValue;
   if (seg_bytes < 0) seg_bytes = chunk_bytes;
   if (seg_bytes % kCopyUnit != 0 || seg_off % 16 != 0 || seg_off + seg_bytes > chunk_bytes)
     return cudaErrorInvalidValue;
   int64_t units = int64_t(n) * (seg_bytes / kCopyUnit);
-  int64_t need = (units + 7) / 8;
+  int64_t need = (units + 8 * kCopyGrab - 1) / (8 * kCopyGrab);  // one grab per warp at least
   grid = int(std::max<int64_t>(1, std::min<int64_t>(grid, need)));
   chunk_copy_kernel<<<grid, 256, 0, s>>>(dst_base, dst_idx, src_base, src_idx, n, chunk_bytes, seg_off,
-                                         seg_bytes);
+                                         seg_bytes, work);
   return cudaGetLastError();
 }
 

@@ -178,6 +178,18 @@ int flush_table(ellm_pool* p, cudaStream_t stream) {
 }
 
 // Upload an int32 array through the staging ring; returns the device pointer.
+// Grid of the SM copy kernels that move chunks over the host link (deflate, inflate, layer-wise
+// offload): one CTA per SM — the room the persistent decode-attention kernel leaves beside it —
+// which already keeps ~4.7 MB of PCIe traffic in flight (measured 51.9 GB/s, the same as with
+// 2 CTAs per SM). ELLM_HOST_COPY_CTAS overrides (experiments).
+int host_copy_grid(const ellm_pool* p) {
+  static const int env = [] {
+    const char* e = std::getenv("ELLM_HOST_COPY_CTAS");
+    return e ? std::atoi(e) : 0;
+  }();
+  return env > 0 ? env : p->num_sms;
+}
+
 int upload_ints(ellm_pool* p, const std::vector<int32_t>& v, cudaStream_t stream,
                 const int32_t** dev, uint64_t* gen) {
   void *h, *d;
@@ -1023,12 +1035,13 @@ int ellm_deflate(ellm_pool* p, int32_t n, const int32_t* ids, int32_t* slots_out
     std::vector<int32_t> both(src);
     both.insert(both.end(), dst.begin(), dst.end());
     const int32_t* dd;
-    int rc = upload_ints(p, both, S(stream), &dd, nullptr);
+    both.push_back(0);  // the copy kernel's work-claim counter
+  int rc = upload_ints(p, both, S(stream), &dd, nullptr);
     if (rc) return rc;
     uint8_t* hdev = nullptr;
     if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&hdev), p->host_slots, 0)) != cudaSuccess)
       return cuda_fail(p, e);
-    if ((e = launch_chunk_copy(hdev, dd + n, pool, dd, n, p->chunk_bytes, 2 * p->num_sms, S(stream))) !=
+    if ((e = launch_chunk_copy(hdev, dd + n, pool, dd, n, p->chunk_bytes, host_copy_grid(p), work_word(dd, 2 * n), S(stream))) !=
         cudaSuccess)
       return cuda_fail(p, e);
     ++p->launches;
@@ -1076,12 +1089,13 @@ int ellm_inflate(ellm_pool* p, int32_t n, const int32_t* slots, int32_t* ids_out
     std::vector<int32_t> both(src);
     both.insert(both.end(), dst.begin(), dst.end());
     const int32_t* dd;
-    int rc = upload_ints(p, both, S(stream), &dd, nullptr);
+    both.push_back(0);  // the copy kernel's work-claim counter
+  int rc = upload_ints(p, both, S(stream), &dd, nullptr);
     if (rc) return rc;
     uint8_t* hdev = nullptr;
     if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&hdev), p->host_slots, 0)) != cudaSuccess)
       return cuda_fail(p, e);
-    if ((e = launch_chunk_copy(pool, dd + n, hdev, dd, n, p->chunk_bytes, 2 * p->num_sms, S(stream))) !=
+    if ((e = launch_chunk_copy(pool, dd + n, hdev, dd, n, p->chunk_bytes, host_copy_grid(p), work_word(dd, 2 * n), S(stream))) !=
         cudaSuccess)
       return cuda_fail(p, e);
     ++p->launches;
@@ -1135,6 +1149,7 @@ int ellm_offload_layer(ellm_pool* p, int32_t layer, int32_t n, const int32_t* id
   for (int32_t i = 0; i < n; ++i)  // the reserved slot may have been read by an inflate elsewhere
     if ((e = wait_freed(p, p->slot_ev, both[size_t(n + i)], S(stream))) != cudaSuccess) return cuda_fail(p, e);
   const int32_t* dd;
+  both.push_back(0);  // the copy kernel's work-claim counter
   int rc = upload_ints(p, both, S(stream), &dd, nullptr);
   if (rc) return rc;
   uint8_t* hdev = nullptr;
@@ -1143,7 +1158,7 @@ int ellm_offload_layer(ellm_pool* p, int32_t layer, int32_t n, const int32_t* id
   // layer l's K and V slabs of all local heads: [2][Hkv][T][d] bf16, contiguous in the chunk
   const int64_t seg = int64_t(4) * p->cfg.n_heads_kv * p->T * p->cfg.head_dim;
   if ((e = launch_chunk_copy(hdev, dd + n, static_cast<uint8_t*>(ellm_vtensor_base(p->vt)), dd, n, p->chunk_bytes,
-                             2 * p->num_sms, S(stream), int64_t(layer) * seg, seg)) != cudaSuccess)
+                             host_copy_grid(p), work_word(dd, 2 * n), S(stream), int64_t(layer) * seg, seg)) != cudaSuccess)
     return cuda_fail(p, e);
   ++p->launches;
   return p->ring.commit(S(stream));
@@ -1206,10 +1221,11 @@ int ellm_migrate(ellm_pool* p, int32_t n, const int32_t* src, const int32_t* dst
   for (int32_t i = 0; i < n; ++i)  // destinations freed by work on another stream
     if ((e = wait_freed(p, p->chunk_ev, dst[i], S(stream))) != cudaSuccess) return cuda_fail(p, e);
   const int32_t* dd;
+  all.push_back(0);  // the copy kernel's work-claim counter
   int rc = upload_ints(p, all, S(stream), &dd, nullptr);
   if (rc) return rc;
   uint8_t* pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
-  e = launch_chunk_copy(pool, dd + n, pool, dd, n, p->chunk_bytes, 2 * p->num_sms, S(stream));
+  e = launch_chunk_copy(pool, dd + n, pool, dd, n, p->chunk_bytes, 2 * p->num_sms, work_word(dd, 2 * n), S(stream));
   if (e != cudaSuccess) return cuda_fail(p, e);
   ++p->launches;
   {  // the source chunks are free once the copy on `stream` is done

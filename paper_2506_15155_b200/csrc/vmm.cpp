@@ -191,7 +191,11 @@ int ellm_vtensor_create(int32_t device, size_t slot_bytes, int64_t n_slots, ellm
   vt->device = device;
   vt->slot_bytes = slot_bytes;
   vt->n_slots = n_slots;
-  if (d.memAddressReserve(&vt->base, slot_bytes * size_t(n_slots), gran, 0, 0) != CUDA_SUCCESS) {
+  // VA aligned to the largest power of two dividing the slot (<= 1 GiB), so the driver may back
+  // large slots with its large page sizes (fewer TLB entries for the attention's scattered reads)
+  size_t align = gran;
+  while (align < (size_t(1) << 30) && slot_bytes % (align * 2) == 0) align *= 2;
+  if (d.memAddressReserve(&vt->base, slot_bytes * size_t(n_slots), align, 0, 0) != CUDA_SUCCESS) {
     delete vt;
     return ELLM_ERR_CUDA;
   }
