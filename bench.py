@@ -38,8 +38,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=None, help="timed steps (default 40; c3: 4 swap rounds)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ellm", "reference"], default="ellm")
-    ap.add_argument("--workload", choices=["c2", "c3", "c4"], default="c2",
-                    help="c2 (default): 8B 32x32K; c3: 8B-262K 16x128K under memory pressure; c4: 70B 64x8K")
+    ap.add_argument("--workload", choices=["c2", "c3", "c4", "c5"], default="c2",
+                    help="c2 (default): 8B 32x32K; c3: 8B-262K 16x128K under memory pressure; c4: 70B 64x8K; "
+                         "c5: 256-request prefill/decode churn with offload, compaction, shrink/grow")
     ap.add_argument("--swap-every", type=int, default=48,
                     help="c3: decode steps per offload/fetch round")
     ap.add_argument("--swap-mode", choices=["sm", "ce", "mixed"], default="ce",
@@ -52,6 +53,8 @@ def parse():
                          "or a separate NCCL all-gather per layer")
     ap.add_argument("--batch", type=int, default=0,
                     help="override the workload's request count (testing; the JSON config records it)")
+    ap.add_argument("--tokens-per-chunk", type=int, default=0,
+                    help="override the workload's tokens per chunk T (layout study; the JSON config records it)")
     ap.add_argument("--no-swap", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -59,7 +62,7 @@ def parse():
                     help="wrap the timed steps in cudaProfilerStart/Stop (ncu --profile-from-start off)")
     a = ap.parse_args()
     if a.steps is None:
-        a.steps = 4 * a.swap_every if a.workload == "c3" else 40
+        a.steps = 4 * a.swap_every if a.workload == "c3" else 128 if a.workload == "c5" else 40
     return a
 
 
@@ -179,6 +182,10 @@ def run_reference(args):
         return
     from inputs import workload as W
     import oracle
+    if args.workload == "c5":
+        print(json.dumps({"impl": "reference", "metric": METRIC,
+                          "unavailable": "c5 is a churn schedule; the oracle arm is defined on c2/c3/c4"}), flush=True)
+        return
     wl = {"c2": W.c2, "c3": W.c3, "c4": W.c4}[args.workload]()
     k, v = W.host_kv(wl, 0, 0, wl.context)
     q = W.host_q(wl, 0, 0)
@@ -225,6 +232,8 @@ def main():
         return run_reference(args)
     if args.workload == "c3":
         return run_c3(args)
+    if args.workload == "c5":
+        return run_c5(args)
     import numpy as np
     import torch
     from paper_2506_15155_b200 import ellm
@@ -249,6 +258,8 @@ def main():
     wl = W.c2(world, rank) if args.workload == "c2" else W.c4(world, rank)
     if args.batch:
         wl.batch = args.batch
+    if args.tokens_per_chunk:
+        wl.tokens_per_chunk = args.tokens_per_chunk
     B, L = wl.batch, wl.n_layers
     swap_chunks = 1024 if not args.no_swap else 0
     t_create = time.perf_counter()
@@ -789,6 +800,166 @@ def run_c3(args):
                    "swap_gbs_bidir_serial": [round(x, 2) for x in swap_gbs],
                    "bytes_per_swap_round": swap_bytes[-1] if swap_bytes else 0,
                    "tokens_per_request": [tokens[r] for r in range(total)],
+                   "pool_create_s": round(t_create, 2)}}
+    print(json.dumps(line), flush=True)
+    pool.close()
+
+
+def run_c5(args):
+    """BASELINE.json configs[4]: 256 requests of the 8B shape with prompts
+    log-uniform in [2K, 128K] and 16-256 output tokens, served by a FIFO loop (inputs/c5.py)
+    over a device pool smaller than the working set: chunked prefill (2048-token slabs: append +
+    tcgen05 prefill attention), decode of every resident request (fused append + attention per
+    layer), offload of the least recently admitted request under pressure and fetch-back,
+    compaction by migration and pool shrink / grow every 64 decode iterations. A step = one
+    scheduler iteration; value = decode tokens/s over exactly K timed iterations (everything
+    the iterations issue is inside the timed region); the c5 object reports prefill tokens/s
+    and the sustained GB/s of every row under churn (CUDA events around each call)."""
+    import numpy as np
+    import torch
+    from paper_2506_15155_b200 import ellm
+    from inputs import workload as W
+    from inputs.c5 import C5Serve, c5_lengths
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        if int(os.environ.get("RANK", "0")) == 0:
+            print(json.dumps({"metric": METRIC, "unavailable": "c5 is a single-GPU configuration"}), flush=True)
+        return
+    torch.cuda.set_device(0)
+    wl = W.c5()
+    n = wl.batch if not args.batch else args.batch
+    prompts, outs = c5_lengths(n, wl.seed)
+    free, _ = torch.cuda.mem_get_info()
+    cb = wl.chunk_bytes()
+    max_chunks = int((free - (10 << 30)) // cb)
+    initial = max_chunks * 3 // 4          # the rest is ACT, grown on demand (pool_grow)
+    host_slots = (48 << 30) // cb
+    t0 = time.perf_counter()
+    pool = ellm.Pool(0, wl.n_layers, wl.hq_local, wl.hkv_local, wl.head_dim, wl.tokens_per_chunk,
+                     max_chunks, initial, n, wl.chunks_per_request, host_slots)
+    t_create = time.perf_counter() - t0
+    pool.set_swap_mode(1)                  # copy engines for offload / fetch
+    pool.set_vmm_overlap(64 << 20, True)   # f1: pre-mapping + asynchronous unmapping
+    cs = torch.cuda.current_stream()
+    srv = C5Serve(pool, wl, prompts, outs, slab=2048, compact_every=64, stream=cs)
+    srv.fast_fill()
+    torch.cuda.synchronize()
+    filled = dict(admitted=srv.count["admitted"], resident_gib=round(pool.stats()["kv_used"] * cb / 2 ** 30, 1))
+    for _ in range(args.warmup):
+        srv.step()
+    torch.cuda.synchronize()
+    srv.ev.clear()
+    c0 = dict(srv.count)
+    launches0 = pool.kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(gpu_id_for(0)) as clk:
+        clk.wait_first_sample()
+        ev0.record(cs)
+        for _ in range(args.steps):
+            srv.step()
+        ev1.record(cs)
+        torch.cuda.synchronize()
+    launches = pool.kernel_launches() - launches0
+    el_ms = ev0.elapsed_time(ev1)
+    dc = {k: srv.count[k] - c0[k] for k in srv.count}
+    value = dc["decode_tokens"] / (el_ms / 1e3)
+    rows = {}
+    for row, e0, e1, amt in srv.ev:
+        ms = e0.elapsed_time(e1)
+        r = rows.setdefault(row, {"calls": 0, "ms": 0.0, "amount": 0})
+        r["calls"] += 1
+        r["ms"] += ms
+        r["amount"] += amt
+    peak, peak_src = hbm_peak()
+    bf16_peak = None
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    bf16_src = None
+    if os.path.exists(mp):  # inside a long step: the sustained (power-capped) GEMM figure
+        j = json.load(open(mp))
+        bf16_peak = j.get("bf16_tflops_sustained") or j.get("bf16_tflops")
+        bf16_src = "measured (MEASURED_PEAKS.json " + (
+            "bf16_tflops_sustained)" if j.get("bf16_tflops_sustained") else "bf16_tflops)")
+    rows_out = {}
+    for row, r in rows.items():
+        o = {"calls": r["calls"], "ms_total": round(r["ms"], 2), "share_of_step": round(r["ms"] / el_ms, 4)}
+        if row == "prefill_attn":
+            tf = r["amount"] / (r["ms"] / 1e3) / 1e12
+            o.update(tflops=round(tf, 1), frac_of_bf16_peak=round(tf / bf16_peak, 4) if bf16_peak else None)
+        else:
+            gbs = r["amount"] / (r["ms"] / 1e3) / 1e9
+            o.update(gbs=round(gbs, 1), bytes=int(r["amount"]))
+            if row in ("deflate", "inflate"):
+                o["bound"] = "host link"
+            else:
+                o["frac_of_hbm"] = round(gbs / peak, 4)
+        rows_out[row] = o
+    dom = max(rows, key=lambda k: rows[k]["ms"]) if rows else None
+    if dom == "prefill_attn" and bf16_peak:
+        a = rows[dom]["amount"] / rows[dom]["calls"] / (rows[dom]["ms"] / rows[dom]["calls"] / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": round(a, 1), "peak": bf16_peak, "unit": "TFLOP/s",
+                "frac": round(a / bf16_peak, 4), "traffic": None,
+                "kernel": "prefill_kernel (ellm_prefill_attention, tcgen05; one launch per layer per slab)",
+                "peak_source": bf16_src}
+    else:
+        r = rows["decode_attn"]
+        a = r["amount"] / (r["ms"] / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(a, 1), "peak": peak, "unit": "GB/s", "frac": round(a / peak, 4),
+                "traffic": None, "kernel": "paged_attn_kernel (ellm_decode_append_attention, one launch per layer)",
+                "alg_bytes_per_launch": int(r["amount"] / r["calls"]), "launch_ms": round(r["ms"] / r["calls"], 4),
+                "peak_source": peak_src}
+    # end to end: the same loop with each iteration's decode Q/K/V copied from pinned host memory
+    # and the attention outputs copied back, inside the timed region
+    e2e = None
+    if not args.no_e2e and srv.running:
+        B = srv.qd.shape[1]
+        srv.host_io = tuple(torch.empty(x.shape, dtype=x.dtype).pin_memory()
+                            for x in (srv.qd, srv.kd, srv.vd, srv.od))
+        srv.events = False
+        n_e2e = 32
+        t_before = srv.count["decode_tokens"]
+        row_b = [0, 0]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(cs)
+        for _ in range(n_e2e):
+            b0 = srv.count["decode_tokens"]
+            srv.step(host=True)
+            nb = srv.count["decode_tokens"] - b0
+            row_b[0] += nb * wl.n_layers * (wl.hq_local + 2 * wl.hkv_local) * wl.head_dim * 2
+            row_b[1] += nb * wl.n_layers * wl.hq_local * wl.head_dim * 2
+        e1.record(cs)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        e2e = {"value": round((srv.count["decode_tokens"] - t_before) / (ems / 1e3), 3), "unit": UNIT,
+               "h2d_bytes_per_step": int(row_b[0] / n_e2e), "d2h_bytes_per_step": int(row_b[1] / n_e2e),
+               "ms_per_step": round(ems / n_e2e, 3), "steps": n_e2e, "max_batch_rows": B}
+    cpu = None
+    mean_len = int(np.mean([srv.lens[r] for r in srv.running])) if srv.running else 32768
+    if not args.no_cpu_baseline:
+        swl = W.Workload(**{**wl.__dict__, "context": mean_len, "batch": 1})
+        per_rl, reps, threads = oracle_sample(swl)
+        cpu = {"value": round(1.0 / (wl.n_layers * per_rl), 4), "unit": UNIT, "cores": threads, "kind": "oracle",
+               "sample": (f"oracle fp64 decode attention of 1 request x 1 layer at the timed window's mean running "
+                          f"context ({mean_len} tokens) repeated {reps}x ({per_rl:.3f} s each); decode tokens/s "
+                          f"extrapolated to {wl.n_layers} layers per token (prefill, swap and compaction excluded)")}
+    st = pool.stats()
+    line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(el_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded lengths; device-generated K/V/Q values)",
+            "config": {**workload_config(wl, 1), "batch": n, "context": "prompts log-uniform 2048-131072, outputs 16-256",
+                       "pool_max_gib": round(max_chunks * cb / 2 ** 30, 1),
+                       "pool_initial_gib": round(initial * cb / 2 ** 30, 1),
+                       "host_slots_gib": round(host_slots * cb / 2 ** 30, 1), "prefill_slab": 2048,
+                       "compact_every": 64, "swap_mode": "ce", "vmm_overlap": "premap 64 MiB + async unmap"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "c5": {"decode_tokens_per_s": round(value, 1),
+                   "prefill_tokens_per_s": round(dc["prefill_tokens"] / (el_ms / 1e3), 1),
+                   "total_tokens_per_s": round((dc["prefill_tokens"] + dc["decode_tokens"]) / (el_ms / 1e3), 1),
+                   "timed_counts": dc, "rows": rows_out, "dominant_row": dom,
+                   "after_fill": filled, "mean_running_context": mean_len,
+                   "running_at_end": len(srv.running), "offloaded_at_end": len(srv.swapped),
+                   "pool_at_end": {k: st[k] for k in ("kv_free", "kv_used", "act", "host_free", "host_used")},
                    "pool_create_s": round(t_create, 2)}}
     print(json.dumps(line), flush=True)
     pool.close()

@@ -104,6 +104,13 @@ def c3(batch=16) -> Workload:
                     tokens_per_chunk=16, decode_headroom=512)
 
 
+def c5(batch=256) -> Workload:
+    """BASELINE.json configs[4]: C5 churn at the LLaMA-3-8B shape: 256 requests, prompts 2K-128K
+    (inputs/c5.py), 2 MiB chunks; the pool is smaller than the working set."""
+    return Workload("c5-churn-8b-256req", 32, 32, 8, 128, batch, 131072, seed=5, tokens_per_chunk=16,
+                    decode_headroom=256, needle=False)
+
+
 def c1() -> Workload:
     return Workload("c1-tiny", 1, 4, 2, 64, 4, 300, seed=0, tokens_per_chunk=16, decode_headroom=64)
 
