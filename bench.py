@@ -55,6 +55,11 @@ def parse():
                     help="override the workload's request count (testing; the JSON config records it)")
     ap.add_argument("--tokens-per-chunk", type=int, default=0,
                     help="override the workload's tokens per chunk T (layout study; the JSON config records it)")
+    ap.add_argument("--layers", type=int, default=0, help="override the layer count (layout study)")
+    ap.add_argument("--context", type=int, default=0, help="override the context length (layout study)")
+    ap.add_argument("--emulate-shard", type=int, default=0,
+                    help="run rank 0's shard of an N-way KV-head split alone on one GPU (no gather): the "
+                         "per-GPU attention rate at the N-GPU geometry, for a box with fewer GPUs")
     ap.add_argument("--no-swap", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -255,11 +260,20 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    wl = W.c2(world, rank) if args.workload == "c2" else W.c4(world, rank)
+    if args.emulate_shard > 1:
+        if world > 1:
+            raise SystemExit("--emulate-shard is a single-process mode")
+        wl = W.c2(args.emulate_shard, 0) if args.workload == "c2" else W.c4(args.emulate_shard, 0)
+    else:
+        wl = W.c2(world, rank) if args.workload == "c2" else W.c4(world, rank)
     if args.batch:
         wl.batch = args.batch
     if args.tokens_per_chunk:
         wl.tokens_per_chunk = args.tokens_per_chunk
+    if args.layers:
+        wl.n_layers = args.layers
+    if args.context:
+        wl.context = args.context
     B, L = wl.batch, wl.n_layers
     swap_chunks = 1024 if not args.no_swap else 0
     t_create = time.perf_counter()
@@ -578,6 +592,9 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (seeded counter-based generator, 3 needles per request/layer/kv-head)",
                 "config": {**workload_config(wl, world),
+                           **({"parallelism": f"rank 0 of a kv-head shard x{args.emulate_shard}, run alone on "
+                                              "1 GPU (no gather): per-GPU rate at that geometry"}
+                              if args.emulate_shard > 1 else {}),
                            **({"gather": "fused attention epilogue, P2P stores into every rank's window"
                                if pg is not None else "NCCL all_gather_into_tensor per layer"} if world > 1 else {})},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
@@ -931,7 +948,10 @@ def run_c5(args):
         ems = e0.elapsed_time(e1)
         e2e = {"value": round((srv.count["decode_tokens"] - t_before) / (ems / 1e3), 3), "unit": UNIT,
                "h2d_bytes_per_step": int(row_b[0] / n_e2e), "d2h_bytes_per_step": int(row_b[1] / n_e2e),
-               "ms_per_step": round(ems / n_e2e, 3), "steps": n_e2e, "max_batch_rows": B}
+               "ms_per_step": round(ems / n_e2e, 3), "steps": n_e2e, "max_batch_rows": B,
+               "note": ("the churn state moves on: these are the 32 iterations after the timed window, "
+                        "with their own running batch and prefill mix; compare ms_per_step and "
+                        "decode tokens per iteration, not only tokens/s")}
     cpu = None
     mean_len = int(np.mean([srv.lens[r] for r in srv.running])) if srv.running else 32768
     if not args.no_cpu_baseline:
