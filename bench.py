@@ -275,7 +275,7 @@ def main():
     if args.context:
         wl.context = args.context
     B, L = wl.batch, wl.n_layers
-    swap_chunks = 1024 if not args.no_swap else 0
+    swap_chunks = min(1024, wl.chunks_per_request) if not args.no_swap else 0
     t_create = time.perf_counter()
     # + one extra request (id = batch) of swap_chunks chunks: the swap / migrate measurements
     # move it between HBM and pinned host memory while the decode set stays resident
@@ -509,12 +509,13 @@ def main():
     t0 = time.perf_counter()
     assert pool.grow(n_vmm) == ellm.OK
     t_grow = time.perf_counter() - t0
+    n_vmm = max(1, n_vmm)
     st1 = pool.stats()
 
     # ---- f1: the caller-side cost of shrink / grow of one default map unit while a
     #      decode step's attention launches are still queued on the GPU — device-synchronising
     #      unmap + on-demand map, vs asynchronous unmapping + speculative pre-mapping ----
-    k_unit = max(1, (64 << 20) // pool.chunk_bytes)
+    k_unit = min(max(1, (64 << 20) // pool.chunk_bytes), pool.stats()["kv_free"])
 
     def vmm_timed(fn):
         for l in range(L):
@@ -530,11 +531,14 @@ def main():
                 "maps": s_after["n_map"] - s_before["n_map"], "unmaps": s_after["n_unmap"] - s_before["n_unmap"]}
 
     f1 = {"chunks": k_unit, "gpu_queue": f"{L} attention launches (~{ms_step:.0f} ms) queued before each call"}
-    f1["sync"] = {"shrink": vmm_timed(lambda: pool.shrink(k_unit)), "grow": vmm_timed(lambda: pool.grow(k_unit))}
-    assert pool.set_vmm_overlap(64 << 20, True) == ellm.OK and pool.vmm_sync() == ellm.OK
-    f1["overlap"] = {"shrink": vmm_timed(lambda: pool.shrink(k_unit)), "grow": vmm_timed(lambda: pool.grow(k_unit)),
-                     "premap_hits": pool.stats()["premap_hits"]}
-    assert pool.set_vmm_overlap(0, False) == ellm.OK and pool.vmm_sync() == ellm.OK
+    if k_unit == 0:
+        f1["skipped"] = "no FREE chunks left in the pool"
+    else:
+        f1["sync"] = {"shrink": vmm_timed(lambda: pool.shrink(k_unit)), "grow": vmm_timed(lambda: pool.grow(k_unit))}
+        assert pool.set_vmm_overlap(64 << 20, True) == ellm.OK and pool.vmm_sync() == ellm.OK
+        f1["overlap"] = {"shrink": vmm_timed(lambda: pool.shrink(k_unit)), "grow": vmm_timed(lambda: pool.grow(k_unit)),
+                         "premap_hits": pool.stats()["premap_hits"]}
+        assert pool.set_vmm_overlap(0, False) == ellm.OK and pool.vmm_sync() == ellm.OK
     torch.cuda.synchronize()
 
     # ---- f4: chunked-prefill attention (tcgen05) over the same chunk-mapped KV: the last

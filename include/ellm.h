@@ -37,7 +37,14 @@
  *
  * Chunk geometry (R1): one chunk = T tokens x L layers x {K,V} x Hkv local
  * kv-heads x d, bf16, layout [L][2][Hkv][T][d]; chunk_bytes = 4*T*L*Hkv*d.
- * Chunk c lives at pool_base + c*chunk_bytes. Table entries: >=0 device chunk id,
+ * Chunk c lives at pool_base + c*chunk_bytes. On the device, layer l's [2][Hkv][T][d] slab sits
+ * in slab slot (l + floor(c/32)) mod L of the chunk ("rotated slabs": consecutive chunks'
+ * slabs of one layer are not at a fixed offset, which costs HBM bandwidth for chunk strides that
+ * are not a power of two); it is used when chunk_bytes is not a power of two, and never when a
+ * chunk is its own map unit (map_unit_bytes == chunk_bytes, the ellm_alias_request
+ * configuration) or for L = 1; ELLM_ROTATE=1 / 0 forces it on / off. Host slots,
+ * ellm_read_chunk and ellm_read_host_slot always hold the canonical image above.
+ * Table entries: >=0 device chunk id,
  * -1 unmapped, <=-2 host slot h encoded as -(h+2).
  */
 #ifndef ELLM_H
@@ -331,7 +338,8 @@ int ellm_get_table(const ellm_pool* pool, int32_t req_id, int32_t* entries, int3
  * ELLM_CHUNK_ACT_SLOT (activation-owned, inside a live activation slot). */
 enum { ELLM_CHUNK_FREE = 0, ELLM_CHUNK_USED = 1, ELLM_CHUNK_ACT = 2, ELLM_CHUNK_ACT_SLOT = 3 };
 int ellm_chunk_states(const ellm_pool* pool, int64_t first, int64_t n, uint8_t* out);
-/* copy chunk_bytes of device chunk `chunk_id` to host_dst (synchronises `stream`). */
+/* copy the canonical [L][2][Hkv][T][d] image (chunk_bytes) of device chunk `chunk_id` to
+ * host_dst, un-rotating its slabs (synchronises `stream`). */
 int ellm_read_chunk(ellm_pool* pool, int64_t chunk_id, void* host_dst, void* stream);
 /* copy chunk_bytes of host slot `slot` to host_dst (synchronises the device). */
 int ellm_read_host_slot(ellm_pool* pool, int64_t slot, void* host_dst);

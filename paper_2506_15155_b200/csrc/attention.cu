@@ -148,6 +148,7 @@ struct Params {
   int64_t W_s, W_d, U, n_dyn;  // static tiles; dynamic tiles; tiles per dynamic unit; units
   int32_t rec_dyn;           // record owner id of dynamic unit 0 (= G + n_vr)
   int32_t table_stride, n_vr, HG, G, T, L, layer, group, Hq;
+  int32_t rot;               // slab rotation (internal.h slab_slot)
   float scale_log2;
   // a10 fused head gather (n_peer > 0; ellm_attention_gather): each merged output row is stored
   // into EVERY rank's gather window over peer memory (NVLink P2P), at global q-head
@@ -292,6 +293,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     s_n_now = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    // PDL: the next attention launch on this stream may be scheduled onto SMs as this grid's
+    // CTAs exit; it streams its K/V before griddepcontrol.wait and does everything that reads
+    // this grid's results or writes memory after it (no-op without the launch attribute)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   }
   __syncthreads();
 
@@ -332,6 +337,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       tk_next2 = atomicAdd(p.ticket, 1ull);
     }
     uint32_t segc = 0;  // segments started (selects the Q slot and its parity)
+    // PDL: the first segment's first NST tiles are issued before griddepcontrol.wait (the K/V of
+    // this layer are not written by the previous launch: pool.cpp only sets the attribute when
+    // that launch did not append into this layer); its Q is staged after the wait, before the
+    // producer could block on a full ring. Fused appends (writes) also wait first.
+    bool waited = false;
+    int issued = 0;
+    auto pdl_wait = [&]() {
+      if (!waited) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        waited = true;
+      }
+    };
     for (;;) {
       int vr = dyn ? uinfo.x : find_vr(cum, p.n_vr, t_begin);
       for (int64_t tile = t_begin; tile < t_end; ++vr) {
@@ -350,13 +367,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             first_dyn_seg ? t_begin - uinfo.y
                           : __ldg(cum + vr) - (dyn ? int64_t(__ldg(p.cum_s + vr + 1) - __ldg(p.cum_s + vr)) : 0);
         const int qs = int(segc % kQSlots);
-        if (lane == 0) {  // stage this segment's Q rows (HB*group x D, contiguous) into its slot
-          mbar_wait(qempty0 + 8 * qs, ((segc / kQSlots) & 1) ^ 1);
-          const uint32_t qbytes = uint32_t(HB * p.group * D * 2);
-          mbar_expect_tx(qfull0 + 8 * qs, qbytes);
-          bulk_load(qbase + qs * QB, p.q + (int64_t(ireq) * p.Hq + hg * HB * p.group) * D, qbytes,
-                    qfull0 + 8 * qs);
-        }
+        auto stage_q = [&]() {
+          if (lane == 0) {  // stage this segment's Q rows (HB*group x D, contiguous) into its slot
+            mbar_wait(qempty0 + 8 * qs, ((segc / kQSlots) & 1) ^ 1);
+            const uint32_t qbytes = uint32_t(HB * p.group * D * 2);
+            mbar_expect_tx(qfull0 + 8 * qs, qbytes);
+            bulk_load(qbase + qs * QB, p.q + (int64_t(ireq) * p.Hq + hg * HB * p.group) * D, qbytes,
+                      qfull0 + 8 * qs);
+          }
+        };
+        bool q_pending = !waited;  // first segment: Q after the first tiles and the PDL wait
+        if (!q_pending) stage_q();
         for (int64_t t = tile; t < seg_end; t += 32) {
           const int cnt = int(min(int64_t(32), seg_end - t));
           int32_t ent[8];
@@ -377,7 +398,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             int32_t e[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) e[k] = __shfl_sync(0xffffffffu, ent[k], u);
+            if (q_pending && issued == NST) {  // the ring is full: Q must be on its way
+              pdl_wait();
+              stage_q();
+              q_pending = false;
+            }
             if (p.k_new != nullptr && (t + u - tile0 + 1) * TT >= len) {
+              pdl_wait();
               // fused decode append: this is the request's last tile, which holds position
               // len-1; write the new K/V rows of heads [hg*HB, hg*HB+HB) into the chunk, then
               // order these generic-proxy stores before the tile's TMA (async proxy) read.
@@ -393,7 +420,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint4* src = kv ? p.v_new : p.k_new;
                 const uint4 val = __ldg(src + (int64_t(ireq) * p.Hkv + hg * HB + h) * PARTS + part);
                 uint8_t* dst = p.pool + int64_t(c) * p.chunk_bytes +
-                               ((int64_t(p.layer * 2 + kv) * p.Hkv + hg * HB + h) * p.T + pos % p.T) * (D * 2) +
+                               ((int64_t(slab_slot(c, p.layer, p.rot) * 2 + kv) * p.Hkv + hg * HB + h) * p.T +
+                                pos % p.T) * (D * 2) +
                                part * 16;
                 *reinterpret_cast<uint4*>(dst) = val;
               }
@@ -416,11 +444,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int k = 0; k < 8; ++k)
                 if (k < npieces && e[k] >= 0)
                   tma_load_5d(sbase + stage * SB + k * piece_bytes, &tmap, 0, 0, tok_in_chunk, hg * HB,
-                              (e[k] * p.L + p.layer) * 2, full0 + 8 * stage, policy);
+                              (e[k] * p.L + slab_slot(e[k], p.layer, p.rot)) * 2, full0 + 8 * stage, policy);
             }
             __syncwarp();
+            ++issued;
             if (++stage == NST) { stage = 0; phase ^= 1; }
           }
+        }
+        if (q_pending) {  // a first segment of fewer than NST tiles
+          pdl_wait();
+          stage_q();
         }
         tile = seg_end;
         ++segc;
@@ -470,6 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   // ========================= consumers =========================
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: before any read of Q or any write
   const int hh = warp % HB, j = warp / HB;
   const int g = lane >> 2, q = lane & 3;
   // smem byte offsets (within a stage) of this lane's K and V reads; fixed for the kernel
@@ -673,9 +707,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 template <int D, int HB>
-cudaError_t launch_t(const CUtensorMap& tmap, const Params& prm, int G, cudaStream_t s) {
-  paged_attn_kernel<D, HB><<<G, kThreads, smem_bytes_for(D), s>>>(tmap, prm);
-  return cudaGetLastError();
+cudaError_t launch_t(const CUtensorMap& tmap, const Params& prm, int G, cudaStream_t s, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem_bytes_for(D);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, paged_attn_kernel<D, HB>, tmap, prm);
 }
 
 }  // namespace
@@ -762,6 +805,7 @@ cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh,
   prm.T = sh.T;
   prm.L = sh.L;
   prm.layer = layer;
+  prm.rot = sh.rot;
   prm.group = sh.group;
   prm.Hq = sh.Hq;
   prm.scale_log2 = scale * 1.4426950408889634f;
@@ -775,17 +819,17 @@ cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh,
   cudaError_t e;
   if (sh.D == 128) {
     switch (sh.HB) {
-      case 1: e = launch_t<128, 1>(tmap, prm, G, s); break;
-      case 2: e = launch_t<128, 2>(tmap, prm, G, s); break;
-      case 4: e = launch_t<128, 4>(tmap, prm, G, s); break;
-      default: e = launch_t<128, 8>(tmap, prm, G, s); break;
+      case 1: e = launch_t<128, 1>(tmap, prm, G, s, plan.pdl); break;
+      case 2: e = launch_t<128, 2>(tmap, prm, G, s, plan.pdl); break;
+      case 4: e = launch_t<128, 4>(tmap, prm, G, s, plan.pdl); break;
+      default: e = launch_t<128, 8>(tmap, prm, G, s, plan.pdl); break;
     }
   } else {
     switch (sh.HB) {
-      case 1: e = launch_t<64, 1>(tmap, prm, G, s); break;
-      case 2: e = launch_t<64, 2>(tmap, prm, G, s); break;
-      case 4: e = launch_t<64, 4>(tmap, prm, G, s); break;
-      default: e = launch_t<64, 8>(tmap, prm, G, s); break;
+      case 1: e = launch_t<64, 1>(tmap, prm, G, s, plan.pdl); break;
+      case 2: e = launch_t<64, 2>(tmap, prm, G, s, plan.pdl); break;
+      case 4: e = launch_t<64, 4>(tmap, prm, G, s, plan.pdl); break;
+      default: e = launch_t<64, 8>(tmap, prm, G, s, plan.pdl); break;
     }
   }
   *launches = e == cudaSuccess ? 1 : 0;

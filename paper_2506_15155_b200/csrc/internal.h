@@ -89,6 +89,22 @@ cudaError_t launch_table_scatter(int32_t* d_table, const TableUpdate* d_updates,
 // a10: wait on `s` until *flag (this rank's gather flag word) >= target (wrapping compare).
 cudaError_t launch_gather_wait(const uint32_t* flag, uint32_t target, uint64_t timeout_ns, cudaStream_t s);
 
+// Rotated slabs: on the device, layer l's [2][Hkv][T][d] slab of chunk c sits in
+// slab slot (l + c / kRotGroup) mod L of the chunk (rot = L), so one layer's slabs of
+// consecutive chunk groups are not all at the same offset a chunk stride apart — with chunk
+// strides of 5 / 10 MiB (70B shape) that pattern loses ~20% of HBM read bandwidth
+// (tools/slab_read.cu). Within an aligned group of kRotGroup chunks the slot is constant, so
+// the prefill kernel's multi-chunk TMA boxes (<= 8 chunks) keep a plain chunk stride and
+// split only at group boundaries (1 tile in 4 at T = 16; 8-chunk groups cost prefill 8%).
+// rot = 0: slot l. Host slots, read_chunk and the oracle keep the canonical image.
+constexpr int32_t kRotGroup = 32;
+__host__ __device__ inline int32_t slab_slot(int64_t c, int32_t l, int32_t rot) {
+  return rot ? int32_t((uint32_t(l) + uint32_t(c) / kRotGroup) % uint32_t(rot)) : l;  // c < 2^31
+}
+__host__ __device__ inline int32_t slab_shift(int64_t c, int32_t rot) {  // slot of layer 0
+  return rot ? int32_t((uint32_t(c) / kRotGroup) % uint32_t(rot)) : 0;
+}
+
 struct AppendDesc {  // device-resident arrays, n entries (+1 for cum)
   const int32_t* req;
   const int32_t* pos0;
@@ -97,7 +113,7 @@ struct AppendDesc {  // device-resident arrays, n entries (+1 for cum)
 cudaError_t launch_kv_append(const AppendDesc& d, int32_t n, int64_t total_rows, const int32_t* table,
                              int32_t table_stride, uint8_t* pool, int64_t chunk_bytes, int32_t T,
                              int32_t layer, int32_t Hkv, int32_t D, const void* k_new,
-                             const void* v_new, int num_sms, cudaStream_t s);
+                             const void* v_new, int num_sms, cudaStream_t s, int32_t rot);
 
 // Chunk copy: dst_base + dst_idx[i]*bytes <- src_base + src_idx[i]*bytes, i < n.
 // (seg_off, seg_bytes): copy only that byte range of each chunk (seg_bytes < 0: whole chunk).
@@ -105,7 +121,10 @@ cudaError_t launch_kv_append(const AppendDesc& d, int32_t n, int64_t total_rows,
 // it with the index lists, so every call has its own).
 cudaError_t launch_chunk_copy(uint8_t* dst_base, const int32_t* dst_idx, const uint8_t* src_base,
                               const int32_t* src_idx, int32_t n, int64_t chunk_bytes, int grid,
-                              uint32_t* work, cudaStream_t s, int64_t seg_off = 0, int64_t seg_bytes = -1);
+                              uint32_t* work, cudaStream_t s, int64_t seg_off = 0, int64_t seg_bytes = -1,
+                              int32_t rot = 0, int64_t slab = 0, bool src_dev = false, bool dst_dev = false);
+// (rot, slab, src_dev, dst_dev): offsets are canonical; a side marked _dev is a pool chunk whose
+// slabs are rotated (slab_slot), the other side (host slot) is canonical.
 inline uint32_t* work_word(const int32_t* uploaded, int64_t index) {
   return reinterpret_cast<uint32_t*>(const_cast<int32_t*>(uploaded + index));
 }
@@ -142,9 +161,14 @@ struct AttnPlan {
   void* gout[kMaxPeers] = {};
   uint32_t* gflag[kMaxPeers] = {};
   int32_t n_peer = 0, Hq_out = 0, q_off = 0;
+  // programmatic dependent launch: this launch may start while the previous kernel on the
+  // stream finishes (attention.cu: K/V streamed before griddepcontrol.wait, all else after)
+  bool pdl = false;
 };
 struct AttnShape {
   int32_t D, HB, HG, Hkv, Hq, group, T, L, TT, nsub;
+  int32_t rot;      // slab rotation (slab_slot): L, or 0 for the canonical layout
+  int64_t slab;     // bytes of one layer's [2][Hkv][T][d] slab
 };
 constexpr int64_t kMaxDynUnits = 4096;   // cap on dynamic units per attention launch
 int attn_heads_per_block(int32_t Hkv);  // HB
@@ -165,6 +189,7 @@ struct alignas(64) PrefillMaps {
   CUtensorMap kv;       // 128-token boxes inside one chunk (T >= 128)
   CUtensorMap run[4];   // boxes of 1/2/4/8 consecutive whole chunks (T < 128)
   CUtensorMap q;
+  int32_t runs;         // 1: run maps usable, 0: none (one box per chunk)
 };
 cudaError_t encode_prefill_kv_maps(PrefillMaps* m, void* pool_base, int64_t max_chunks, const AttnShape& sh,
                                    int64_t chunk_bytes);
@@ -292,6 +317,10 @@ struct ellm_pool {
   int64_t g_win_bytes = 0;
   std::vector<uint32_t> g_expect;
   uint64_t g_timeout_ns = 20000000000ull;
+
+  // programmatic dependent launch of attention (attention.cu; ELLM_PDL=0 turns it off)
+  bool pdl = true;
+  int32_t last_fused_layer = -1;     // layer the previous attention launch appended into, or -1
 
   std::map<int32_t, std::pair<CUdeviceptr, size_t>> alias;
   int last_cuda_error = 0;

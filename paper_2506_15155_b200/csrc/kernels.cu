@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(256) kv_append_kernel(
     const int32_t* __restrict__ req, const int32_t* __restrict__ pos0,
     const int32_t* __restrict__ cum_rows, int32_t n, int64_t total_rows, const int32_t* __restrict__ table,
     int32_t table_stride, uint8_t* __restrict__ pool, int64_t chunk_bytes, int32_t T, int32_t layer,
-    int32_t Hkv, int32_t parts, const uint4* __restrict__ k_new, const uint4* __restrict__ v_new) {
+    int32_t Hkv, int32_t parts, const uint4* __restrict__ k_new, const uint4* __restrict__ v_new, int32_t rot) {
   const int lane = threadIdx.x & 31;
   const int units = Hkv * parts;  // 16-byte units per row and kv
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
@@ -40,7 +40,8 @@ __global__ void __launch_bounds__(256) kv_append_kernel(
     }
     const int32_t p = __ldg(pos0 + lo) + int32_t(row - __ldg(cum_rows + lo));
     const int32_t c = __ldg(table + int64_t(__ldg(req + lo)) * table_stride + p / T);
-    uint8_t* kdst = pool + int64_t(c) * chunk_bytes + (int64_t(layer * 2) * Hkv * T + (p % T)) * parts * 16;
+    uint8_t* kdst =
+        pool + int64_t(c) * chunk_bytes + (int64_t(slab_slot(c, layer, rot) * 2) * Hkv * T + (p % T)) * parts * 16;
     uint8_t* vdst = kdst + int64_t(Hkv) * T * parts * 16;
     const uint4* ksrc = k_new + row * units;
     const uint4* vsrc = v_new + row * units;
@@ -77,7 +78,8 @@ __global__ void __launch_bounds__(256) chunk_copy_kernel(uint8_t* __restrict__ d
                                                          const uint8_t* __restrict__ src_base,
                                                          const int32_t* __restrict__ src_idx,
                                                          int32_t n, int64_t chunk_bytes, int64_t seg_off,
-                                                         int64_t seg_bytes, uint32_t* __restrict__ work) {
+                                                         int64_t seg_bytes, uint32_t* __restrict__ work,
+                                                         int32_t rot, int64_t slab, bool src_dev, bool dst_dev) {
   // Work is claimed dynamically (one atomic per 64 KiB) rather than by a static grid stride: a
   // swap usually runs beside the persistent attention kernel, which leaves room for one copy
   // CTA per SM, so with a static split the CTAs that only become resident after the first
@@ -95,9 +97,17 @@ __global__ void __launch_bounds__(256) chunk_copy_kernel(uint8_t* __restrict__ d
     const int64_t u1 = u0 + kCopyGrab < total ? u0 + kCopyGrab : total;
     for (int64_t w = u0; w < u1; ++w) {
       const int64_t i = w / units_per_chunk;
-      const int64_t off = seg_off + (w % units_per_chunk) * kCopyUnit;
-      const uint4* s = reinterpret_cast<const uint4*>(src_base + int64_t(__ldg(src_idx + i)) * chunk_bytes + off);
-      uint4* d = reinterpret_cast<uint4*>(dst_base + int64_t(__ldg(dst_idx + i)) * chunk_bytes + off);
+      const int64_t off = seg_off + (w % units_per_chunk) * kCopyUnit;  // canonical offset
+      const int64_t cs = __ldg(src_idx + i), cd = __ldg(dst_idx + i);
+      int64_t soff = off, doff = off;
+      if (rot) {  // a pool side holds layer l's slab in slot slab_slot(c, l)
+        const int32_t l = int32_t(off / slab);
+        const int64_t in = off - int64_t(l) * slab;
+        if (src_dev) soff = int64_t(slab_slot(cs, l, rot)) * slab + in;
+        if (dst_dev) doff = int64_t(slab_slot(cd, l, rot)) * slab + in;
+      }
+      const uint4* s = reinterpret_cast<const uint4*>(src_base + cs * chunk_bytes + soff);
+      uint4* d = reinterpret_cast<uint4*>(dst_base + cd * chunk_bytes + doff);
       uint4 v[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) v[k] = __ldcs(s + k * 32 + lane);
@@ -120,30 +130,32 @@ cudaError_t launch_table_scatter(int32_t* d_table, const TableUpdate* d_updates,
 cudaError_t launch_kv_append(const AppendDesc& d, int32_t n, int64_t total_rows, const int32_t* table,
                              int32_t table_stride, uint8_t* pool, int64_t chunk_bytes, int32_t T,
                              int32_t layer, int32_t Hkv, int32_t D, const void* k_new,
-                             const void* v_new, int num_sms, cudaStream_t s) {
+                             const void* v_new, int num_sms, cudaStream_t s, int32_t rot) {
   const int32_t parts = D / 8;
   if (Hkv * parts > 32 * kAppendMaxPerLane) return cudaErrorInvalidValue;
   const int64_t blocks = (total_rows + 7) / 8;  // 8 warps (rows) per block
   int grid = int(std::min<int64_t>(blocks, int64_t(num_sms) * 8));
   kv_append_kernel<<<grid, 256, 0, s>>>(d.req, d.pos0, d.cum_rows, n, total_rows, table, table_stride,
                                         pool, chunk_bytes, T, layer, Hkv, parts,
-                                        static_cast<const uint4*>(k_new), static_cast<const uint4*>(v_new));
+                                        static_cast<const uint4*>(k_new), static_cast<const uint4*>(v_new), rot);
   return cudaGetLastError();
 }
 
 cudaError_t launch_chunk_copy(uint8_t* dst_base, const int32_t* dst_idx, const uint8_t* src_base,
                               const int32_t* src_idx, int32_t n, int64_t chunk_bytes, int grid,
-                              uint32_t* work, cudaStream_t s, int64_t seg_off, int64_t seg_bytes) {
+                              uint32_t* work, cudaStream_t s, int64_t seg_off, int64_t seg_bytes, int32_t rot,
+                              int64_t slab, bool src_dev, bool dst_dev) {
   if (n <= 0) return cudaSuccess;
   if (work == nullptr) return cudaErrorInvalidValue;
   if (seg_bytes < 0) seg_bytes = chunk_bytes;
   if (seg_bytes % kCopyUnit != 0 || seg_off % 16 != 0 || seg_off + seg_bytes > chunk_bytes)
     return cudaErrorInvalidValue;
+  if (rot && (slab % kCopyUnit != 0 || seg_off % kCopyUnit != 0)) return cudaErrorInvalidValue;
   int64_t units = int64_t(n) * (seg_bytes / kCopyUnit);
   int64_t need = (units + 8 * kCopyGrab - 1) / (8 * kCopyGrab);  // one grab per warp at least
   grid = int(std::max<int64_t>(1, std::min<int64_t>(grid, need)));
   chunk_copy_kernel<<<grid, 256, 0, s>>>(dst_base, dst_idx, src_base, src_idx, n, chunk_bytes, seg_off,
-                                         seg_bytes, work);
+                                         seg_bytes, work, rot, slab, src_dev, dst_dev);
   return cudaGetLastError();
 }
 

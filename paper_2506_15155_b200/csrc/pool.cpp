@@ -91,15 +91,34 @@ cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 // Copy-engine path of deflate / inflate: dst_base[dst[i]] <- src_base[src[i]], chunk_bytes each,
 // as ONE cudaMemcpyBatchAsync (host cost independent of the chunk count; copies prefer to
 // overlap with compute). Falls back to one cudaMemcpyAsync per chunk if the batch API fails.
+// With rotated slabs (rot = L) the pool side of chunk c holds canonical layers [0, L-r) at slots
+// [r, L) and [L-r, L) at [0, r), r = slab_shift(c): two copies per chunk (dev_side: 1 = src,
+// 2 = dst).
 cudaError_t ce_copy(uint8_t* dst_base, const std::vector<int32_t>& dst, const uint8_t* src_base,
-                    const std::vector<int32_t>& src, int64_t chunk_bytes, cudaStream_t stream) {
-  const size_t n = dst.size();
-  std::vector<void*> d(n), s(n);
-  std::vector<size_t> sz(n, size_t(chunk_bytes));
-  for (size_t i = 0; i < n; ++i) {
-    d[i] = dst_base + int64_t(dst[i]) * chunk_bytes;
-    s[i] = const_cast<uint8_t*>(src_base) + int64_t(src[i]) * chunk_bytes;
+                    const std::vector<int32_t>& src, int64_t chunk_bytes, cudaStream_t stream,
+                    int32_t rot = 0, int64_t slab = 0, int dev_side = 0) {
+  std::vector<void*> d, s;
+  std::vector<size_t> sz;
+  for (size_t i = 0; i < dst.size(); ++i) {
+    uint8_t* dc = dst_base + int64_t(dst[i]) * chunk_bytes;
+    uint8_t* sc = const_cast<uint8_t*>(src_base) + int64_t(src[i]) * chunk_bytes;
+    const int64_t r = slab_shift(dev_side == 1 ? src[i] : dst[i], rot);
+    if (r == 0) {
+      d.push_back(dc), s.push_back(sc), sz.push_back(size_t(chunk_bytes));
+      continue;
+    }
+    uint8_t* canon = dev_side == 1 ? dc : sc;  // canonical side
+    uint8_t* dev = dev_side == 1 ? sc : dc;
+    uint8_t* a[2] = {canon, canon + (rot - r) * slab};          // layers [0, L-r), [L-r, L)
+    uint8_t* b[2] = {dev + r * slab, dev};                      // slots  [r, L),   [0, r)
+    const size_t len[2] = {size_t((rot - r) * slab), size_t(r * slab)};
+    for (int k = 0; k < 2; ++k) {
+      d.push_back(dev_side == 1 ? a[k] : b[k]);
+      s.push_back(dev_side == 1 ? b[k] : a[k]);
+      sz.push_back(len[k]);
+    }
   }
+  const size_t n = d.size();
   cudaMemcpyAttributes attr;
   std::memset(&attr, 0, sizeof(attr));
   attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
@@ -478,6 +497,16 @@ int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out) {
   a.nsub = a.TT / 16;
   a.T = T;
   a.L = c.n_layers;
+  // rotated slabs (internal.h slab_slot): used when the chunk stride is not a
+  // power of two (power-of-two strides read at full rate canonically, and the rotation costs the
+  // prefill kernel ~8%), and possible unless a chunk is its own map unit (ellm_alias_request's
+  // contiguous per-request view needs the canonical image), the layer count is 1, or a slab is
+  // not a whole number of 4 KiB copy units. ELLM_ROTATE=1 / 0 forces it on / off.
+  a.slab = p->chunk_bytes / c.n_layers;
+  const bool can_rot = c.n_layers > 1 && p->chunks_per_unit > 1 && a.slab % 4096 == 0;
+  bool want_rot = (p->chunk_bytes & (p->chunk_bytes - 1)) != 0;
+  if (const char* v = std::getenv("ELLM_ROTATE")) want_rot = std::atoi(v) != 0;
+  a.rot = (can_rot && want_rot) ? c.n_layers : 0;
   // split-K partial records: pid < (G + n_vr) * nsub, each [HB*group][D] fp32 + (m, l)
   p->part_records = (int64_t(p->num_sms) + 2 * int64_t(c.max_requests) * a.HG + kMaxDynUnits) * a.nsub;
   if ((e = cudaMalloc(reinterpret_cast<void**>(&p->d_part),
@@ -494,6 +523,7 @@ int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out) {
   if ((e = encode_kv_tensor_map(&p->tmap, ellm_vtensor_base(p->vt), c.max_chunks, a)) != cudaSuccess)
     return fail(cuda_fail(p, e));
   if ((e = attn_configure(a.D, a.HB)) != cudaSuccess) return fail(cuda_fail(p, e));
+  if (const char* v = std::getenv("ELLM_PDL")) p->pdl = std::atoi(v) != 0;
   *out = p;
   return ELLM_OK;
 }
@@ -651,7 +681,7 @@ int ellm_kv_append(ellm_pool* p, int32_t layer, int32_t n, const int32_t* reqs,
   cudaError_t e = launch_kv_append(ad, n, rows, p->d_table, p->cfg.max_chunks_per_request,
                                    static_cast<uint8_t*>(ellm_vtensor_base(p->vt)), p->chunk_bytes,
                                    p->T, layer, p->cfg.n_heads_kv, p->cfg.head_dim, k_new, v_new,
-                                   p->num_sms, S(stream));
+                                   p->num_sms, S(stream), p->ash.rot);
   if (e != cudaSuccess) return cuda_fail(p, e);
   ++p->launches;
   return p->ring.commit(S(stream));
@@ -950,6 +980,13 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
       plan.gflag[i] = reinterpret_cast<uint32_t*>(p->g_win[size_t(i)]) + layer;
     }
   }
+  // PDL (attention.cu): only without dynamic tickets (shared counter), with a full grid (one
+  // CTA per SM, so at most this launch and the previous one overlap: a third could start only
+  // once all of this one's CTAs are resident, i.e. once the first has exited everywhere), and
+  // when the previous launch of this pool did not append into this layer (its K/V rows may
+  // still be in flight when this launch streams the layer before griddepcontrol.wait)
+  plan.pdl = p->pdl && plan.n_dyn == 0 && plan.G == p->num_sms && p->last_fused_layer != layer;
+  p->last_fused_layer = k_new ? layer : -1;
   int launches = 0;
   cudaError_t e = launch_paged_attention(p->tmap, a, ad, n, n_vr, plan, p->d_table,
                                          p->cfg.max_chunks_per_request, layer, q, out, p->d_part,
@@ -1029,7 +1066,8 @@ int ellm_deflate(ellm_pool* p, int32_t n, const int32_t* ids, int32_t* slots_out
     if ((e = wait_freed(p, p->slot_ev, h, S(stream))) != cudaSuccess) return cuda_fail(p, e);
   uint8_t* pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
   if (p->swap_mode == 1) {
-    if ((e = ce_copy(p->host_slots, dst, pool, src, p->chunk_bytes, S(stream))) != cudaSuccess)
+    if ((e = ce_copy(p->host_slots, dst, pool, src, p->chunk_bytes, S(stream), p->ash.rot, p->ash.slab, 1)) !=
+        cudaSuccess)
       return cuda_fail(p, e);
   } else {
     std::vector<int32_t> both(src);
@@ -1041,8 +1079,8 @@ int ellm_deflate(ellm_pool* p, int32_t n, const int32_t* ids, int32_t* slots_out
     uint8_t* hdev = nullptr;
     if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&hdev), p->host_slots, 0)) != cudaSuccess)
       return cuda_fail(p, e);
-    if ((e = launch_chunk_copy(hdev, dd + n, pool, dd, n, p->chunk_bytes, host_copy_grid(p), work_word(dd, 2 * n), S(stream))) !=
-        cudaSuccess)
+    if ((e = launch_chunk_copy(hdev, dd + n, pool, dd, n, p->chunk_bytes, host_copy_grid(p), work_word(dd, 2 * n), S(stream),
+                               0, -1, p->ash.rot, p->ash.slab, true, false)) != cudaSuccess)
       return cuda_fail(p, e);
     ++p->launches;
   }
@@ -1083,7 +1121,8 @@ int ellm_inflate(ellm_pool* p, int32_t n, const int32_t* slots, int32_t* ids_out
     if ((e = wait_freed(p, p->chunk_ev, c, S(stream))) != cudaSuccess) return cuda_fail(p, e);
   uint8_t* pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
   if (p->swap_mode == 1) {
-    if ((e = ce_copy(pool, dst, p->host_slots, src, p->chunk_bytes, S(stream))) != cudaSuccess)
+    if ((e = ce_copy(pool, dst, p->host_slots, src, p->chunk_bytes, S(stream), p->ash.rot, p->ash.slab, 2)) !=
+        cudaSuccess)
       return cuda_fail(p, e);
   } else {
     std::vector<int32_t> both(src);
@@ -1095,8 +1134,8 @@ int ellm_inflate(ellm_pool* p, int32_t n, const int32_t* slots, int32_t* ids_out
     uint8_t* hdev = nullptr;
     if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&hdev), p->host_slots, 0)) != cudaSuccess)
       return cuda_fail(p, e);
-    if ((e = launch_chunk_copy(pool, dd + n, hdev, dd, n, p->chunk_bytes, host_copy_grid(p), work_word(dd, 2 * n), S(stream))) !=
-        cudaSuccess)
+    if ((e = launch_chunk_copy(pool, dd + n, hdev, dd, n, p->chunk_bytes, host_copy_grid(p), work_word(dd, 2 * n), S(stream),
+                               0, -1, p->ash.rot, p->ash.slab, false, true)) != cudaSuccess)
       return cuda_fail(p, e);
     ++p->launches;
   }
@@ -1158,7 +1197,8 @@ int ellm_offload_layer(ellm_pool* p, int32_t layer, int32_t n, const int32_t* id
   // layer l's K and V slabs of all local heads: [2][Hkv][T][d] bf16, contiguous in the chunk
   const int64_t seg = int64_t(4) * p->cfg.n_heads_kv * p->T * p->cfg.head_dim;
   if ((e = launch_chunk_copy(hdev, dd + n, static_cast<uint8_t*>(ellm_vtensor_base(p->vt)), dd, n, p->chunk_bytes,
-                             host_copy_grid(p), work_word(dd, 2 * n), S(stream), int64_t(layer) * seg, seg)) != cudaSuccess)
+                             host_copy_grid(p), work_word(dd, 2 * n), S(stream), int64_t(layer) * seg, seg,
+                             p->ash.rot, p->ash.slab, true, false)) != cudaSuccess)
     return cuda_fail(p, e);
   ++p->launches;
   return p->ring.commit(S(stream));
@@ -1225,7 +1265,8 @@ int ellm_migrate(ellm_pool* p, int32_t n, const int32_t* src, const int32_t* dst
   int rc = upload_ints(p, all, S(stream), &dd, nullptr);
   if (rc) return rc;
   uint8_t* pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
-  e = launch_chunk_copy(pool, dd + n, pool, dd, n, p->chunk_bytes, 2 * p->num_sms, work_word(dd, 2 * n), S(stream));
+  e = launch_chunk_copy(pool, dd + n, pool, dd, n, p->chunk_bytes, 2 * p->num_sms, work_word(dd, 2 * n), S(stream), 0,
+                        -1, p->ash.rot, p->ash.slab, true, true);
   if (e != cudaSuccess) return cuda_fail(p, e);
   ++p->launches;
   {  // the source chunks are free once the copy on `stream` is done
@@ -1524,8 +1565,13 @@ int ellm_read_chunk(ellm_pool* p, int64_t c, void* host_dst, void* stream) {
   if (p->owner[size_t(c)] != KV) return ELLM_ERR_NOT_MAPPED;
   cudaError_t e;
   const uint8_t* src = static_cast<const uint8_t*>(ellm_vtensor_base(p->vt)) + c * p->chunk_bytes;
-  if ((e = cudaMemcpyAsync(host_dst, src, size_t(p->chunk_bytes), cudaMemcpyDeviceToHost, S(stream))) !=
-          cudaSuccess ||
+  // the canonical [L][2][Hkv][T][d] image: layer l from slab slot slab_slot(c, l)
+  const int64_t r = slab_shift(c, p->ash.rot), sl = p->ash.slab;
+  uint8_t* dst = static_cast<uint8_t*>(host_dst);
+  if ((e = cudaMemcpyAsync(dst, src + r * sl, size_t(p->chunk_bytes - r * sl), cudaMemcpyDeviceToHost,
+                           S(stream))) != cudaSuccess ||
+      (r > 0 && (e = cudaMemcpyAsync(dst + (p->chunk_bytes - r * sl), src, size_t(r * sl), cudaMemcpyDeviceToHost,
+                                     S(stream))) != cudaSuccess) ||
       (e = cudaStreamSynchronize(S(stream))) != cudaSuccess)
     return cuda_fail(p, e);
   return ELLM_OK;

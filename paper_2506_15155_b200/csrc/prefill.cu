@@ -156,6 +156,8 @@ struct PParams {
   const int32_t* table;
   __nv_bfloat16* out;      // [rows][Hq][D]
   int32_t table_stride, Hq, group, T, L, layer, Hkv;
+  int32_t rot;             // slab rotation (internal.h slab_slot)
+  int32_t runs;            // run maps usable (else one box per chunk through maps.kv)
   float scale_log2;
 };
 
@@ -233,27 +235,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t dst = sb + LY::off_kv + s * 2 * LY::TILE + kv * LY::TILE;
       // runs of consecutive chunk ids go as one box of 1/2/4/8 chunks (TMA issue cost is per box)
       const int prev = __shfl_up_sync(0xffffffffu, e, 1);
-      unsigned starts = __ballot_sync(0xffffffffu, lane < npc && (lane == 0 || e != prev + 1 || p.T >= kN));
+      // with rotated slabs a run also breaks at a rotation-group boundary (the slot changes there)
+      unsigned starts = __ballot_sync(
+          0xffffffffu, lane < npc && (lane == 0 || e != prev + 1 || p.T >= kN || !p.runs ||
+                                      (p.rot && e % kRotGroup == 0)));
       if (lane == 0) {
         mbar_wait(empty, ((t >> 1) & 1) ^ 1);
         mbar_expect_tx(full, uint32_t(npc * tp * 128 * HALVES));
       }
-      const int lh = (p.layer * 2 + kv) * p.Hkv + kvh;
       while (starts) {
         const int k = __ffs(starts) - 1;
         starts &= starts - 1;
         const int kend = starts ? __ffs(starts) - 1 : npc;
         const int c = __shfl_sync(0xffffffffu, e, k);
         if (lane == 0) {
-          if (p.T >= kN) {  // one 128-token box inside one chunk
+          const int sl = slab_slot(c, p.layer, p.rot);
+          if (p.T >= kN || !p.runs) {  // one box inside one chunk (128 tokens, or the chunk's T)
             for (int h = 0; h < HALVES; ++h)
-              tma_5d(dst + h * kN * 128, &maps.kv, 0, (t * kN) % p.T, h, kvh, (c * p.L + p.layer) * 2 + kv, full,
-                     policy);
+              tma_5d(dst + h * kN * 128 + k * tp * 128, &maps.kv, 0, p.T >= kN ? (t * kN) % p.T : 0, h, kvh,
+                     (c * p.L + sl) * 2 + kv, full, policy);
           } else {
+            // run map dim 3: (kv, head) blocks over the whole pool; dim 4 steps one chunk (+ one
+            // slab when rotated: consecutive chunks' slots advance by one) — see encode below
+            const int c3 = (sl * 2 + kv) * p.Hkv + kvh;  // the run's slot: constant inside it
             for (int done = 0; done < kend - k;) {
               const int lg = min(3, 31 - __clz(kend - k - done));
               for (int h = 0; h < HALVES; ++h)
-                tma_5d(dst + h * kN * 128 + (k + done) * tp * 128, &maps.run[lg], 0, 0, h, lh, c + done, full,
+                tma_5d(dst + h * kN * 128 + (k + done) * tp * 128, &maps.run[lg], 0, 0, h, c3, c + done, full,
                        policy);
               done += 1 << lg;
             }
@@ -457,7 +465,9 @@ cudaError_t encode_prefill_kv_maps(PrefillMaps* m, void* pool_base, int64_t max_
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  // runs of consecutive chunks: {64, T, d/64, (layer*2 + kv)*Hkv + head, chunk}; box 1/2/4/8 chunks
+  // runs of consecutive chunks (inside one rotation group when slabs are rotated):
+  // {64, T, d/64, (slot*2 + kv)*Hkv + head, chunk}; box 1/2/4/8 chunks
+  m->runs = 0;
   for (int lg = 0; lg < 4; ++lg) {
     cuuint64_t dims[5] = {64, cuuint64_t(sh.T), cuuint64_t(halves), cuuint64_t(sh.L) * 2 * sh.Hkv,
                           cuuint64_t(max_chunks)};
@@ -466,8 +476,9 @@ cudaError_t encode_prefill_kv_maps(PrefillMaps* m, void* pool_base, int64_t max_
     if (d.tensorMapEncodeTiled(&m->run[lg], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, pool_base, dims, strides, box, es,
                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return cudaErrorInvalidValue;
+      return cudaSuccess;  // no run maps: one box per chunk through m->kv (runs = 0)
   }
+  m->runs = 1;
   return cudaSuccess;
 }
 
@@ -501,6 +512,8 @@ cudaError_t launch_prefill_attention(const PrefillMaps& maps, const AttnShape& s
   prm.Hkv = sh.Hkv;
   prm.L = sh.L;
   prm.layer = layer;
+  prm.rot = sh.rot;
+  prm.runs = maps.runs;
   prm.scale_log2 = scale * 1.4426950408889634f;
   if (n_work == 0) return cudaSuccess;
   return sh.D == 128 ? launch_d<128>(maps, prm, n_work, s) : launch_d<64>(maps, prm, n_work, s);
