@@ -320,9 +320,13 @@ def main():
             reserve_s.append(time.perf_counter() - t0)
         if rc:
             raise ellm.EllmError(rc, "reserve")
+        # world == 1, fused: one event pair around the L back-to-back launches (an event between
+        # two launches would keep the next from overlapping the previous one's tail, PDL), so the
+        # per-launch time is the span / L; otherwise one pair per launch
+        span = fused and pg is None and gath is None
         for l in range(L):
             if fused:  # kv_append + attention + split-K merge in one launch per layer
-                if record:
+                if record and (not span or l == 0):
                     e0 = torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
                 if pg is not None:  # ... + the head gather (a10) in the same launch
@@ -348,10 +352,10 @@ def main():
                     rc = pool.attention(l, reqs, q[l], out[l], scale, sp)
                 if rc:
                     raise ellm.EllmError(rc, "attention")
-            if record:
+            if record and (not span or l == L - 1):
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(stream)
-                attn_ev.append((e0, e1))
+                attn_ev.append((e0, e1, L if span else 1))
             if pg is not None:  # the layer's consumer waits for every rank's rows
                 rc = pool.gather_wait(l, sp)
                 if rc:
@@ -383,7 +387,7 @@ def main():
             torch.cuda.profiler.stop()
     launches = pool.kernel_launches() - launches0
     el_ms = ev0.elapsed_time(ev1)
-    attn_ms = [a.elapsed_time(b) for a, b in attn_ev]
+    attn_ms = [a.elapsed_time(b) / k for a, b, k in attn_ev]
     if dist:
         t = torch.tensor([el_ms, statistics.mean(attn_ms)], device="cpu" if same_gpu else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

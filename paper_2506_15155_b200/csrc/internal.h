@@ -56,6 +56,8 @@ class StagingRing {
   void touch(const void* dev);
   // Record that work enqueued on `stream` so far consumes every touched segment.
   int commit(cudaStream_t stream);
+  // Same, but the event is recorded later on `stream` (next commit, or before reuse).
+  int commit_lazy(cudaStream_t stream);
   bool still_valid(const void* dev, uint64_t generation) const;
   size_t seg_bytes() const { return seg_bytes_; }
 
@@ -67,6 +69,8 @@ class StagingRing {
   };
   int retire_and_advance();
   int commit_seg(int seg, cudaStream_t stream);
+  int flush_pending(int only_seg);  // -1: all
+  std::vector<std::pair<int, cudaStream_t>> pending_;
   std::vector<int> touched_;
   uint8_t* h_ = nullptr;
   uint8_t* d_ = nullptr;

@@ -850,8 +850,9 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
     key[size_t(i)] = reqs[i];
     key[size_t(n + i)] = int32_t(p->len[size_t(reqs[i])]);
   }
-  if (key != p->cache_key || p->cache_epoch != p->table_epoch ||
-      !p->ring.still_valid(p->cache_dev, p->cache_gen)) {
+  const bool upload = key != p->cache_key || p->cache_epoch != p->table_epoch ||
+                      !p->ring.still_valid(p->cache_dev, p->cache_gen);
+  if (upload) {
     // layout: req[n] len[n] cum_s[n_vr+1] cum_d[n_vr+1] b_first[n_vr] b_last[n_vr]
     //         u_first[n_vr] u_last[n_vr] dyn_info[n_dyn][8] dyn_ent[n_dyn][U * npieces]
     std::vector<int32_t> d(size_t(2 * n + 6 * n_vr + 2));
@@ -997,7 +998,7 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
   if (plan.n_dyn > 0) p->ticket_base += uint64_t(plan.n_dyn) + 2 * uint64_t(plan.G);
   // every rank merges its n_vr requests once and adds them to every rank's flag word
   if (gather_off >= 0) p->g_expect[size_t(layer)] += uint32_t(p->g_world) * uint32_t(n_vr);
-  return p->ring.commit(S(stream));
+  return upload ? p->ring.commit(S(stream)) : p->ring.commit_lazy(S(stream));
 }
 
 extern "C" {

@@ -87,6 +87,7 @@ void StagingRing::destroy() {
 int StagingRing::retire_and_advance() {
   cur_ = (cur_ + 1) % n_segs_;
   off_ = 0;
+  if (int rc = flush_pending(cur_)) return rc;
   Seg& s = segs_[size_t(cur_)];
   for (auto e : s.events) {  // the segment's previous consumers must be done
     if (cudaEventSynchronize(e) != cudaSuccess) return ELLM_ERR_CUDA;
@@ -127,11 +128,38 @@ int StagingRing::upload(void* dev, size_t bytes, cudaStream_t stream) {
 }
 
 int StagingRing::commit(cudaStream_t stream) {
+  if (int rc = flush_pending(-1)) return rc;
   for (int seg : touched_) {
     int rc = commit_seg(seg, stream);
     if (rc) return rc;
   }
   touched_.clear();
+  return ELLM_OK;
+}
+
+// Work that only re-reads an uploaded segment (an attention launch whose descriptors are
+// cached) records no event now — an event between two attention launches would stop the
+// second from overlapping the first (PDL). The event is recorded on the same stream later:
+// at the next eager commit, or before the segment is reused; it then also covers this work.
+int StagingRing::commit_lazy(cudaStream_t stream) {
+  for (int seg : touched_) {
+    bool have = false;
+    for (auto& ps : pending_) have |= (ps.first == seg && ps.second == stream);
+    if (!have) pending_.emplace_back(seg, stream);
+  }
+  touched_.clear();
+  return ELLM_OK;
+}
+
+int StagingRing::flush_pending(int only_seg) {
+  for (size_t i = 0; i < pending_.size();) {
+    if (only_seg >= 0 && pending_[i].first != only_seg) {
+      ++i;
+      continue;
+    }
+    if (int rc = commit_seg(pending_[i].first, pending_[i].second)) return rc;
+    pending_.erase(pending_.begin() + long(i));
+  }
   return ELLM_OK;
 }
 
