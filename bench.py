@@ -297,8 +297,17 @@ def main():
     CONC_STEPS = 30 if swap_chunks else 0  # decode steps with a concurrent swap stream (15 per mode)
     e2e_steps += CONC_STEPS
     e2e_steps += UNFUSED_STEPS
-    inputs = []
-    for s in range(n_steps + e2e_steps):
+    # distinct per-step inputs in a ring capped at ~2 GiB (the 70B shape's 105 MB per step would
+    # not fit beside its 165 GiB pool otherwise); values only feed traffic here, parity is tests/
+    per_step = L * B * (wl.hq_local + 2 * wl.hkv_local) * wl.head_dim * 2
+    n_ring = int(min(n_steps + e2e_steps, max(8, (2 << 30) // per_step)))
+
+    class _Ring(list):
+        def __getitem__(self, i):
+            return list.__getitem__(self, i % len(self)) if isinstance(i, int) else list.__getitem__(self, i)
+
+    inputs = _Ring()
+    for s in range(n_ring):
         inputs.append(W.decode_inputs(wl, s, lens + s))
     out = torch.empty((L, B, wl.hq_local, wl.head_dim), dtype=torch.bfloat16, device="cuda")
     p2p = world > 1 and args.gather == "p2p"
@@ -421,8 +430,8 @@ def main():
     e2e = None
     n_e2e = e2e_steps - UNFUSED_STEPS - CONC_STEPS
     if n_e2e:
-        hin = []
-        for s in range(n_steps, n_steps + n_e2e):
+        hin = _Ring()
+        for s in range(n_steps, n_steps + min(n_e2e, n_ring)):
             hin.append(tuple(x.cpu().pin_memory() for x in inputs[s]))
         dq, dk, dv = (torch.empty_like(x) for x in inputs[0])
         if pg is not None:  # the result of a step is the gathered [L, B, Hq, d] output
@@ -434,7 +443,8 @@ def main():
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for hq, hk, hv in hin:
+        for j in range(n_e2e):
+            hq, hk, hv = hin[j]
             dq.copy_(hq, non_blocking=True)
             dk.copy_(hk, non_blocking=True)
             dv.copy_(hv, non_blocking=True)

@@ -48,3 +48,20 @@ def test_sharded_heads_draw_same_values():
     k_all, _ = gen.request_kv(1, 0, 40, 0, range(8), 128, 4, needle_range=40)
     k_sh, _ = gen.request_kv(1, 0, 40, 0, range(4, 6), 128, 4, needle_range=40)
     assert np.array_equal(k_all[:, 4:6], k_sh)
+
+
+def test_c5_length_mix_recipe():
+    """BASELINE.json configs[4] length mix (inputs/c5.py): prompts log-uniform in [2K, 128K],
+    outputs uniform in [16, 256], deterministic per seed."""
+    import numpy as np
+    from inputs.c5 import c5_lengths
+    p, o = c5_lengths(256, 5)
+    p2, o2 = c5_lengths(256, 5)
+    assert np.array_equal(p, p2) and np.array_equal(o, o2)
+    assert p.min() >= 2048 and p.max() <= 131072 and o.min() >= 16 and o.max() <= 256
+    # log-uniform: log2 of the prompts is ~uniform on [11, 17]; mean of a log-uniform on
+    # [a, b] is (b - a) / ln(b / a) = 30.5K
+    lg = np.log2(p)
+    assert abs(lg.mean() - 14.0) < 0.35
+    assert 24000 < p.mean() < 37000
+    assert not np.array_equal(c5_lengths(256, 6)[0], p)
