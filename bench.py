@@ -1032,9 +1032,10 @@ def measure_swap(pool, wl, stream):
             assert rc == ellm.OK, rc
             best_d2h = max(best_d2h, n * cb / t / 1e9)
             src = pool.table(1)[0][:n].tolist()
-            t, rc = timed(lambda: pool.migrate(src, sorted(ids), sp))
+            nm = len(src)
+            t, rc = timed(lambda: pool.migrate(src, sorted(ids)[:nm], sp))
             assert rc == ellm.OK, rc
-            best_mig = max(best_mig, 2 * n * cb / t / 1e9)
+            best_mig = max(best_mig, 2 * nm * cb / t / 1e9)
             t, (rc, back) = timed(lambda: pool.inflate(slots, sp))
             assert rc == ellm.OK, rc
             best_h2d = max(best_h2d, n * cb / t / 1e9)
