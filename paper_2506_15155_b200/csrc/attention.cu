@@ -243,11 +243,18 @@ __device__ __forceinline__ void merge_request(const Params& p, int vr, int rows,
 }
 
 // largest vr with cum[vr] <= t
+// The largest vr with cum[vr] <= t (cum non-decreasing, cum[0] = 0 <= t), found by the whole
+// warp: each round the 32 lanes probe evenly spaced entries and the bracket shrinks 32x, so a
+// CTA's first lookup costs ceil(log32 n_vr) dependent loads instead of log2 n_vr (launch ramp).
 __device__ __forceinline__ int find_vr(const int32_t* cum, int n_vr, int64_t t) {
-  int lo = 0, hi = n_vr - 1;
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (__ldg(cum + mid) <= t) lo = mid; else hi = mid - 1;
+  const int lane = threadIdx.x & 31;
+  int lo = 0, hi = n_vr;  // answer in [lo, hi)
+  while (hi - lo > 1) {
+    const int step = (hi - lo + 31) >> 5;
+    const int idx = lo + lane * step;
+    const unsigned le = __ballot_sync(0xffffffffu, idx < hi && __ldg(cum + idx) <= t);
+    lo += (31 - __clz(le)) * step;  // lane 0 always qualifies (cum[lo] <= t)
+    hi = min(hi, lo + step);
   }
   return lo;
 }
