@@ -325,6 +325,7 @@ struct ellm_pool {
   // programmatic dependent launch of attention (attention.cu; ELLM_PDL=0 turns it off)
   bool pdl = true;
   int32_t last_fused_layer = -1;     // layer the previous attention launch appended into, or -1
+  int32_t prev_fused_layer = -1;     // the same for the launch before it
 
   std::map<int32_t, std::pair<CUdeviceptr, size_t>> alias;
   int last_cuda_error = 0;

@@ -986,7 +986,11 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
   // once all of this one's CTAs are resident, i.e. once the first has exited everywhere), and
   // when the previous launch of this pool did not append into this layer (its K/V rows may
   // still be in flight when this launch streams the layer before griddepcontrol.wait)
-  plan.pdl = p->pdl && plan.n_dyn == 0 && plan.G == p->num_sms && p->last_fused_layer != layer;
+  // (the launch before that is also checked: under SM contention from other streams its last
+  // CTA can outlive the previous launch's start-up)
+  plan.pdl = p->pdl && plan.n_dyn == 0 && plan.G == p->num_sms && p->last_fused_layer != layer &&
+             p->prev_fused_layer != layer;
+  p->prev_fused_layer = p->last_fused_layer;
   p->last_fused_layer = k_new ? layer : -1;
   int launches = 0;
   cudaError_t e = launch_paged_attention(p->tmap, a, ad, n, n_vr, plan, p->d_table,
