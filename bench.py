@@ -283,6 +283,9 @@ def main():
                        extra_requests=1 if swap_chunks else 0)
     t_create = time.perf_counter() - t_create
     st_create = pool.stats()
+    # the decode step issues the L attention launches back to back: let each overlap the
+    # previous one's tail (PDL)
+    pool.set_launch_overlap(True)
     prefill_appends = []
     W.prefill(pool, wl, append_times=prefill_appends)
     if swap_chunks:

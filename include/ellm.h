@@ -257,6 +257,16 @@ int ellm_pool_shrink(ellm_pool* pool, int64_t n);
 int ellm_set_vmm_overlap(ellm_pool* pool, int64_t premap_bytes, int32_t async_unmap);
 int ellm_vmm_sync(ellm_pool* pool);
 
+/* Launch overlap between consecutive attention calls of this pool on one stream (programmatic
+ * dependent launch): with enable = 1 a full-grid attention launch may start on
+ * SMs the previous attention launch has left, streaming its layer's K/V before it waits for
+ * that launch; everything else (Q, appends, outputs, split-K workspace) follows the wait. For
+ * callers that issue a model's layers back to back; a caller that records events or issues
+ * other work between attention calls gains nothing from it (and was measured slower in the C5
+ * churn loop), hence off by default. ELLM_PDL=0/1 in the environment overrides. INVALID_ARG
+ * for enable not in {0,1}; NO_DEVICE on a host-only pool. */
+int ellm_set_launch_overlap(ellm_pool* pool, int32_t enable);
+
 /* ---- activation eTensors in the unified pool --------------
  * act_alloc: an activation tensor slot of ceil(bytes / chunk_bytes) consecutive ACT chunks
  *   that are not inside another slot — the run with the highest last chunk id (activations

@@ -322,8 +322,9 @@ struct ellm_pool {
   std::vector<uint32_t> g_expect;
   uint64_t g_timeout_ns = 20000000000ull;
 
-  // programmatic dependent launch of attention (attention.cu; ELLM_PDL=0 turns it off)
-  bool pdl = true;
+  // programmatic dependent launch of attention (attention.cu; ellm_set_launch_overlap, ELLM_PDL)
+  bool pdl = false;
+  bool pdl_env = false;              // ELLM_PDL set: the environment wins over the setter
   int32_t last_fused_layer = -1;     // layer the previous attention launch appended into, or -1
   int32_t prev_fused_layer = -1;     // the same for the launch before it
 

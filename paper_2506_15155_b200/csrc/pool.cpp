@@ -523,7 +523,10 @@ int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out) {
   if ((e = encode_kv_tensor_map(&p->tmap, ellm_vtensor_base(p->vt), c.max_chunks, a)) != cudaSuccess)
     return fail(cuda_fail(p, e));
   if ((e = attn_configure(a.D, a.HB)) != cudaSuccess) return fail(cuda_fail(p, e));
-  if (const char* v = std::getenv("ELLM_PDL")) p->pdl = std::atoi(v) != 0;
+  if (const char* v = std::getenv("ELLM_PDL")) {
+    p->pdl = std::atoi(v) != 0;
+    p->pdl_env = true;
+  }
   *out = p;
   return ELLM_OK;
 }
@@ -1515,6 +1518,13 @@ int ellm_prefill_attention(ellm_pool* p, int32_t layer, int32_t n, const int32_t
   if (e != cudaSuccess) return cuda_fail(p, e);
   ++p->launches;
   return p->ring.commit(st);
+}
+
+int ellm_set_launch_overlap(ellm_pool* p, int32_t enable) {
+  if (!p || (enable != 0 && enable != 1)) return ELLM_ERR_INVALID_ARG;
+  if (!p->has_dev) return ELLM_ERR_NO_DEVICE;
+  if (!p->pdl_env) p->pdl = enable != 0;
+  return ELLM_OK;
 }
 
 int ellm_set_vmm_overlap(ellm_pool* p, int64_t premap_bytes, int32_t async_unmap) {

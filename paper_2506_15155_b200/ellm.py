@@ -77,6 +77,7 @@ _SIGS = {
     "ellm_pool_shrink": (ctypes.c_int, [_P, _I64]),
     "ellm_set_swap_mode": (ctypes.c_int, [_P, _I32]),
     "ellm_set_vmm_overlap": (ctypes.c_int, [_P, ctypes.c_int64, _I32]),
+    "ellm_set_launch_overlap": (ctypes.c_int, [_P, _I32]),
     "ellm_vmm_sync": (ctypes.c_int, [_P]),
     "ellm_prefill_attention": (ctypes.c_int, [_P, _I32, _I32, _P, _P, _P, _P, ctypes.c_float, _P]),
     "ellm_act_alloc": (ctypes.c_int, [_P, ctypes.c_int64, _P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_P)]),
@@ -269,6 +270,10 @@ class Pool:
     def set_vmm_overlap(self, premap_bytes: int = 0, async_unmap: bool = False) -> int:
         """f1: speculative pre-mapping budget and asynchronous unmapping."""
         return ellm_set_vmm_overlap(self._h, int(premap_bytes), int(bool(async_unmap)))
+
+    def set_launch_overlap(self, enable: bool = True) -> int:
+        """PDL between back-to-back attention launches of this pool (off by default)."""
+        return ellm_set_launch_overlap(self._h, int(bool(enable)))
 
     def vmm_sync(self) -> int:
         return ellm_vmm_sync(self._h)

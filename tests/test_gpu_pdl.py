@@ -24,6 +24,7 @@ def test_back_to_back_attention_sequences(pdl, monkeypatch):
     MC = 4096 // T
     C = R * MC
     t = Twin(L, Hq, Hkv, d, T, C, C, R, MC, 0, seed=21)
+    assert t.p.set_launch_overlap(True) == 0   # the environment (ELLM_PDL) wins over it
     reqs = list(range(R))
     assert t.reserve(reqs, lens) == 0
     t.append_all_layers(reqs, lens)
