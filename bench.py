@@ -325,8 +325,7 @@ def main():
     sp = stream.cuda_stream
     attn_ev, app_ev, reserve_s = [], [], []
 
-    def step(q, k, v, record=False, fused=True, o=None):
-        out_ = out if o is None else o
+    def step(q, k, v, record=False, fused=True):
         t0 = time.perf_counter()
         rc = pool.reserve(reqs, ones, sp)
         if record:
@@ -345,7 +344,7 @@ def main():
                 if pg is not None:  # ... + the head gather (a10) in the same launch
                     rc = pool.attention_gather(l, reqs, q[l], pg.offset(l), scale, k[l], v[l], sp)
                 else:
-                    rc = pool.decode_append_attention(l, reqs, k[l], v[l], q[l], out_[l], scale, sp)
+                    rc = pool.decode_append_attention(l, reqs, k[l], v[l], q[l], out[l], scale, sp)
                 if rc:
                     raise ellm.EllmError(rc, "decode_append_attention")
             else:
@@ -362,7 +361,7 @@ def main():
                 if pg is not None:
                     rc = pool.attention_gather(l, reqs, q[l], pg.offset(l), scale, None, None, sp)
                 else:
-                    rc = pool.attention(l, reqs, q[l], out_[l], scale, sp)
+                    rc = pool.attention(l, reqs, q[l], out[l], scale, sp)
                 if rc:
                     raise ellm.EllmError(rc, "attention")
             if record and (not span or l == L - 1):
@@ -374,7 +373,7 @@ def main():
                 if rc:
                     raise ellm.EllmError(rc, "gather_wait")
             elif gath is not None:
-                dist.all_gather_into_tensor(gath[l], out_[l])
+                dist.all_gather_into_tensor(gath[l], out[l])
 
     def barrier():
         torch.cuda.synchronize()
@@ -447,51 +446,16 @@ def main():
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        if pg is None:
-            # pipelined through the public calls: a copy stream uploads step j+1's Q/K/V and
-            # downloads step j's outputs while step j computes (double-buffered device inputs
-            # and outputs, event-ordered); every byte still crosses the host link in the region
-            cst = torch.cuda.Stream()
-            dev = [(dq, dk, dv), tuple(torch.empty_like(x) for x in inputs[0])]
-            outs = [out, torch.empty_like(out)]
-            houts = [hout, torch.empty(out.shape, dtype=out.dtype).pin_memory()]
-            ready = [torch.cuda.Event(), torch.cuda.Event()]
-            done = [torch.cuda.Event(), torch.cuda.Event()]     # step j computed
-            dl_done = [torch.cuda.Event(), torch.cuda.Event()]  # step j's outputs downloaded
-
-            def upload(j):
-                b = j % 2
-                with torch.cuda.stream(cst):
-                    if j >= 2:
-                        cst.wait_event(done[b])          # step j-2 no longer reads these inputs
-                    for dt, ht in zip(dev[b], hin[j]):
-                        dt.copy_(ht, non_blocking=True)
-                    ready[b].record(cst)
-
-            cst.wait_stream(stream)
-            upload(0)
-            for j in range(n_e2e):
-                b = j % 2
-                if j + 1 < n_e2e:
-                    upload(j + 1)
-                stream.wait_event(ready[b])
-                if j >= 2:
-                    stream.wait_event(dl_done[b])         # step j-2's outputs are downloaded
-                step(*dev[b], o=outs[b])
-                done[b].record(stream)
-                with torch.cuda.stream(cst):
-                    cst.wait_event(done[b])
-                    houts[b].copy_(outs[b], non_blocking=True)
-                    dl_done[b].record(cst)
-            stream.wait_stream(cst)
-        else:
-            for j in range(n_e2e):
-                hq, hk, hv = hin[j]
-                dq.copy_(hq, non_blocking=True)
-                dk.copy_(hk, non_blocking=True)
-                dv.copy_(hv, non_blocking=True)
-                step(dq, dk, dv)
+        for j in range(n_e2e):
+            hq, hk, hv = hin[j]
+            dq.copy_(hq, non_blocking=True)
+            dk.copy_(hk, non_blocking=True)
+            dv.copy_(hv, non_blocking=True)
+            step(dq, dk, dv)
+            if pg is not None:
                 ellm.memcpy_async(hout.data_ptr(), pg.out(0), d2h, sp)
+            else:
+                hout.copy_(out, non_blocking=True)
         e1.record(stream)
         barrier()
         ems = e0.elapsed_time(e1)
