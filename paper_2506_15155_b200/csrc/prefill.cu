@@ -30,7 +30,8 @@ namespace {
 
 constexpr int kM = 128;         // MMA rows per CTA
 constexpr int kN = 128;         // keys per tile
-constexpr int kStages = 2;      // K/V ring depth
+constexpr int kKStages = 3;     // K ring depth: K(t+2) is requested while S(t) / softmax(t) run
+constexpr int kVStages = 2;     // V ring depth
 constexpr int kThreads = 192;   // warp 0 TMA, warp 1 MMA, warps 2..5 softmax
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleHeadroom = 8.f;  // log2 units: P <= 2^8 before O is rescaled
@@ -41,9 +42,10 @@ struct Layout {
   static constexpr int Q = kM * D * 2;     // [D/64][128 rows][64]
   static constexpr int P = kM * kN * 2;    // one P buffer: [2 token halves][128 rows][64]
   static constexpr int off_q = 0;
-  static constexpr int off_kv = Q;         // stage s: K at off_kv + 2*s*TILE, V at + TILE
-  static constexpr int off_p = off_kv + kStages * 2 * TILE;
-  static constexpr int off_bar = off_p + 2 * P;  // P double-buffered
+  static constexpr int off_k = Q;          // K stage s at off_k + s*TILE
+  static constexpr int off_v = off_k + kKStages * TILE;  // V stage s at off_v + s*TILE
+  static constexpr int off_p = off_v + kVStages * TILE;
+  static constexpr int off_bar = off_p + P;  // one P buffer (its reuse waits for P.V of the tile before)
   // >= 116 KB so one CTA owns an SM (its 512 TMEM columns are the whole TMEM)
   static constexpr int bytes = (off_bar + 256 + 1024) > 118784 ? (off_bar + 256 + 1024) : 118784;
 };
@@ -170,13 +172,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sb = smem_u32(smem);
   const uint32_t bar0 = sb + LY::off_bar;
-  // barriers: q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2],
+  // barriers: q_full, k_full[3], k_empty[3], v_full[2], v_empty[2], s_full[2], p_full[2],
   // pv_done[2]; then the TMEM address. K and V slots are released separately (K(t) right after
-  // S(t)); P is double-buffered, so the softmax of tile t+1 overlaps P.V of tile t and waits for
-  // it only when it must rescale O.
-  const uint32_t q_full = bar0, k_full = bar0 + 8, k_empty = bar0 + 24, v_full = bar0 + 40,
-                 v_empty = bar0 + 56, s_full = bar0 + 72, p_full = bar0 + 88, pv_done = bar0 + 104;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + LY::off_bar + 128);
+  // S(t)); the K ring is 3 deep so K(t+2) is in flight during softmax(t) (ncu: softmax warps
+  // waited on S, i.e. on K from L2, with a 2-deep ring). The single P buffer is rewritten once
+  // P.V of the previous tile has read it; the exponentials are computed before that wait.
+  const uint32_t q_full = bar0, k_full = bar0 + 8, k_empty = bar0 + 32, v_full = bar0 + 56,
+                 v_empty = bar0 + 72, s_full = bar0 + 88, p_full = bar0 + 104, pv_done = bar0 + 120;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + LY::off_bar + 192);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int4 w0 = p.work[2 * blockIdx.x], w1 = p.work[2 * blockIdx.x + 1];
@@ -186,9 +189,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kKStages; ++s) {
       mbar_init(k_full + 8 * s, 1);
       mbar_init(k_empty + 8 * s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(v_full + 8 * s, 1);
       mbar_init(v_empty + 8 * s, 1);
       mbar_init(s_full + 8 * s, 1);
@@ -227,12 +232,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto load_ent = [&](int t) {
       return (t < n_tiles && lane < pieces(t)) ? __ldg(trow + (t * kN + lane * tp) / p.T) : -1;
     };
-    // order: K(0), K(1), V(0), K(2), V(1), ... — K runs one tile ahead of V
+    // order: K(0), K(1), K(2), V(0), K(3), V(1), ... — K runs two tiles ahead of V
     auto issue = [&](int t, int kv, int e) {
-      const int s = t & 1;
+      const int s = kv ? (t & 1) : (t % kKStages);
+      const int round = kv ? (t >> 1) : (t / kKStages);
       const uint32_t full = (kv ? v_full : k_full) + 8 * s, empty = (kv ? v_empty : k_empty) + 8 * s;
       const int npc = pieces(t);
-      const uint32_t dst = sb + LY::off_kv + s * 2 * LY::TILE + kv * LY::TILE;
+      const uint32_t dst = sb + (kv ? LY::off_v : LY::off_k) + s * LY::TILE;
       // runs of consecutive chunk ids go as one box of 1/2/4/8 chunks (TMA issue cost is per box)
       const int prev = __shfl_up_sync(0xffffffffu, e, 1);
       // with rotated slabs a run also breaks at a rotation-group boundary (the slot changes there)
@@ -240,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           0xffffffffu, lane < npc && (lane == 0 || e != prev + 1 || p.T >= kN || !p.runs ||
                                       (p.rot && e % kRotGroup == 0)));
       if (lane == 0) {
-        mbar_wait(empty, ((t >> 1) & 1) ^ 1);
+        mbar_wait(empty, (round & 1) ^ 1);
         mbar_expect_tx(full, uint32_t(npc * tp * 128 * HALVES));
       }
       while (starts) {
@@ -270,14 +276,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
     };
-    int e_cur = load_ent(0), e_next = load_ent(1);
+    int e_cur = load_ent(0), e_n1 = load_ent(1), e_n2 = load_ent(2);
     issue(0, 0, e_cur);
+    if (n_tiles > 1) issue(1, 0, e_n1);
     for (int t = 0; t < n_tiles; ++t) {
-      const int e_after = load_ent(t + 2);  // in flight while this iteration waits
-      if (t + 1 < n_tiles) issue(t + 1, 0, e_next);
+      const int e_after = load_ent(t + 3);  // in flight while this iteration waits
+      if (t + 2 < n_tiles) issue(t + 2, 0, e_n2);
       issue(t, 1, e_cur);
-      e_cur = e_next;
-      e_next = e_after;
+      e_cur = e_n1;
+      e_n1 = e_n2;
+      e_n2 = e_after;
     }
   } else if (warp == 1) {
     // ================================ MMA issuer ================================
@@ -286,17 +294,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t id_pv = idesc_bf16(kM, D, true);
       mbar_wait(q_full, 0);
       auto issue_s = [&](int t) {
-        const int s = t & 1;
-        mbar_wait(k_full + 8 * s, (t >> 1) & 1);
+        const int s = t & 1, ks = t % kKStages;
+        mbar_wait(k_full + 8 * ks, (t / kKStages) & 1);
         tc_fence_after();
-        const uint32_t kb = sb + LY::off_kv + s * 2 * LY::TILE;
+        const uint32_t kb = sb + LY::off_k + ks * LY::TILE;
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * (kM * 128) + (k & 3) * 32;
           umma(tmem + s * 128, desc_sw128(sb + LY::off_q + off, 16), desc_sw128(kb + off, 16), id_s, k > 0);
         }
         umma_commit(s_full + 8 * s);
-        umma_commit(k_empty + 8 * s);
+        umma_commit(k_empty + 8 * ks);
       };
       issue_s(0);
       for (int t = 0; t < n_tiles; ++t) {
@@ -304,10 +312,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(p_full + 8 * (t & 1), (t >> 1) & 1);
         mbar_wait(v_full + 8 * (t & 1), (t >> 1) & 1);
         tc_fence_after();
-        const uint32_t vb = sb + LY::off_kv + (t & 1) * 2 * LY::TILE + LY::TILE;
+        const uint32_t vb = sb + LY::off_v + (t & 1) * LY::TILE;
 #pragma unroll
         for (int k = 0; k < kN / 16; ++k)
-          umma(tmem + 256, desc_sw128(sb + LY::off_p + (t & 1) * LY::P + (k >> 2) * (kM * 128) + (k & 3) * 32, 16),
+          umma(tmem + 256, desc_sw128(sb + LY::off_p + (k >> 2) * (kM * 128) + (k & 3) * 32, 16),
                desc_sw128(vb + k * 2048, kN * 128), id_pv, (t > 0 || k > 0) ? 1u : 0u);
         umma_commit(v_empty + 8 * (t & 1));
         umma_commit(pv_done + 8 * (t & 1));
@@ -367,18 +375,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_wait_st();
       }
       if (grow) m_run = m_tile;
-      if (t >= 2) mbar_wait(pv_done + 8 * (t & 1), ((t >> 1) - 1) & 1);  // P buffer of tile t-2 read
-      uint8_t* pbase = prow_base + (t & 1) * LY::P;
       float sm[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 independent partial sums
       const float neg_m = -m_run;
 #pragma unroll
-      for (int c16 = 0; c16 < kN / 8; ++c16) {  // 16-byte chunk = 8 tokens
-        float pv[8];
+      for (int j = 0; j < kN; ++j) {  // exponentials first (in place), before the P-buffer wait
+        x[j] = ex2(fmaf(x[j], p.scale_log2, neg_m));
+        sm[j & 7] += x[j];
+      }
+      if (t >= 1) mbar_wait(pv_done + 8 * ((t - 1) & 1), ((t - 1) >> 1) & 1);  // P.V(t-1) read P
+      uint8_t* pbase = prow_base;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          pv[e] = ex2(fmaf(x[c16 * 8 + e], p.scale_log2, neg_m));
-          sm[e] += pv[e];
-        }
+      for (int c16 = 0; c16 < kN / 8; ++c16) {  // 16-byte chunk = 8 tokens
+        const float* pv = x + c16 * 8;
         const int half = c16 >> 3, ch = c16 & 7;
         uint4 v;
         v.x = pack_bf16(pv[0], pv[1]);
@@ -391,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (t == n_tiles - 1) {  // V rows past the last visible key may hold anything: zero them
         const int need = last_key + 1 - t * kN;
         if (row >= need) {
-          uint8_t* vrow = smem + LY::off_kv + (t & 1) * 2 * LY::TILE + LY::TILE + row * 128;
+          uint8_t* vrow = smem + LY::off_v + (t & 1) * LY::TILE + row * 128;
 #pragma unroll
           for (int h = 0; h < HALVES; ++h)
 #pragma unroll
