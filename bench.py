@@ -585,6 +585,65 @@ def main():
           "flops": "4*d*sum_i(P_i+1)*Hq (causal, algorithmic)", "peak_source": "MEASURED_PEAKS.json bf16_tflops"}
     del pf_q, pf_out
 
+    # ---- f2: layer-wise offload during prefill. The extra request (16K tokens) is
+    #      prefilled layer by layer (one causal prefill-attention launch over all its positions per
+    #      layer) with and without offloading each finished layer's slabs on a second stream; the
+    #      exposed delay is what the O(N) offload adds to the O(N^2) prefill. Fetched back after. ----
+    f2 = None
+    if swap_chunks and world == 1:
+        X = wl.batch
+        ids = pool.table(X)[0].tolist()
+        nX = int(pool.table(X)[1])
+        nq = nX  # the whole request is prefilled (causal), layer by layer
+        f2q = torch.randn((nq, wl.hq_local, wl.head_dim), generator=qg, device="cuda", dtype=torch.bfloat16)
+        f2o = torch.empty_like(f2q)
+        side = torch.cuda.Stream()
+
+        def layers(offload):
+            torch.cuda.synchronize()
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            if offload:
+                side.wait_event(c0)
+                s0.record(side)
+            for l in range(L):
+                assert pool.prefill_attention(l, [X], [nq], f2q, f2o, scale, sp) == ellm.OK
+                if offload:
+                    e = torch.cuda.Event()
+                    e.record(stream)
+                    side.wait_event(e)
+                    assert pool.offload_layer(l, ids, side.cuda_stream) == ellm.OK
+            if offload:
+                s1.record(side)
+                stream.wait_stream(side)
+            c1.record(stream)
+            torch.cuda.synchronize()
+            return c0.elapsed_time(c1), (s0.elapsed_time(s1) if offload else 0.0)
+
+        layers(False)  # warm
+        t_compute, _ = layers(False)
+        off_bytes = len(ids) * pool.chunk_bytes
+        f2 = {"request_tokens": nX, "chunks": len(ids), "offload_bytes": off_bytes, "n_q_per_layer": nq,
+              "compute_ms": round(t_compute, 3),
+              "note": "offload of layer l (second stream) follows that layer's causal prefill attention over "
+                      "the whole request; sm = SM copy kernel, ce = DMA copy engines"}
+        for mode, name in ((0, "sm"), (1, "ce")):
+            pool.set_swap_mode(mode)
+            ids = pool.table(X)[0].tolist()
+            rc, f2_slots = pool.offload_begin(ids)
+            assert rc == ellm.OK, rc
+            t_both, t_side = layers(True)
+            assert pool.offload_commit(ids, sp) == ellm.OK
+            rc, _ = pool.inflate([-e - 2 for e in pool.table(X)[0].tolist()], sp)  # host slot h is -(h+2)
+            assert rc == ellm.OK, rc
+            torch.cuda.synchronize()
+            f2[name] = {"compute_plus_offload_ms": round(t_both, 3), "exposed_ms": round(t_both - t_compute, 3),
+                        "offload_stream_ms": round(t_side, 3),
+                        "offload_gbs": round(off_bytes / (t_side / 1e3) / 1e9, 2)}
+        pool.set_swap_mode(0)
+        del f2q, f2o
+
     rows = {
         "a1_pool_create": {"s": round(t_create, 3), "chunks_mapped": st_create["n_map"],
                            "map_us_per_chunk": round(st_create["map_ns"] / max(1, st_create["n_map"]) / 1e3, 2),
@@ -600,6 +659,7 @@ def main():
                                 "map_us_per_chunk": round((st1["map_ns"] - st0["map_ns"]) / max(1, n_vmm) / 1e3, 2)},
         "f1_vmm_overlap": f1,
         "f4_prefill": f4,
+        "f2_layerwise_offload": f2,
     }
 
     cpu = None

@@ -214,8 +214,10 @@ int ellm_inflate(ellm_pool* pool, int32_t n, const int32_t* host_slots, int32_t*
  *   already being offloaded -> ALREADY_MAPPED.
  * offload_layer: copy layer `layer`'s K/V slabs (2*Hkv*T*d*2 contiguous bytes per chunk) of the
  *   listed chunks to their reserved slots on `stream` — call it right after that layer's
- *   kv_append so the copy overlaps the following layers. Chunk not being offloaded ->
- *   NOT_MAPPED. Appends into an offloading chunk after its layer was copied are not carried.
+ *   kv_append so the copy overlaps the following layers. The copy runs on the SM copy kernel,
+ *   or as one cudaMemcpyBatchAsync on the DMA copy engines when ellm_set_swap_mode(1) (no SMs
+ *   taken from the compute it overlaps). Chunk not being offloaded -> NOT_MAPPED. Appends into
+ *   an offloading chunk after its layer was copied are not carried.
  * offload_commit: every layer of every listed chunk copied (else INVALID_ARG): repoint the
  *   table entries to the slots and free the chunks — the same end state (tables, slots, bytes)
  *   as ellm_deflate of the same list. */

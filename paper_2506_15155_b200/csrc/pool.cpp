@@ -1195,6 +1195,33 @@ int ellm_offload_layer(ellm_pool* p, int32_t layer, int32_t n, const int32_t* id
   cudaError_t e;
   for (int32_t i = 0; i < n; ++i)  // the reserved slot may have been read by an inflate elsewhere
     if ((e = wait_freed(p, p->slot_ev, both[size_t(n + i)], S(stream))) != cudaSuccess) return cuda_fail(p, e);
+  // layer l's K and V slabs of all local heads: [2][Hkv][T][d] bf16, contiguous in the chunk
+  const int64_t seg = int64_t(4) * p->cfg.n_heads_kv * p->T * p->cfg.head_dim;
+  uint8_t* pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
+  if (p->swap_mode == 1) {  // copy engines (no SMs taken from the prefill compute): one batch
+    const size_t nn = static_cast<size_t>(n);
+    std::vector<void*> d(nn), src(nn);
+    std::vector<size_t> sz(nn, static_cast<size_t>(seg));
+    for (int32_t i = 0; i < n; ++i) {
+      const int64_t c = ids[i], h = both[size_t(n + i)];
+      src[size_t(i)] = pool + c * p->chunk_bytes + int64_t(slab_slot(c, layer, p->ash.rot)) * seg;
+      d[size_t(i)] = p->host_slots + h * p->chunk_bytes + int64_t(layer) * seg;
+    }
+    cudaMemcpyAttributes attr;
+    std::memset(&attr, 0, sizeof(attr));
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+    size_t attr_idx = 0, fail_idx = 0;
+    e = cudaMemcpyBatchAsync(d.data(), src.data(), sz.data(), size_t(n), &attr, &attr_idx, 1, &fail_idx, S(stream));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      for (int32_t i = 0; i < n; ++i)
+        if ((e = cudaMemcpyAsync(d[size_t(i)], src[size_t(i)], sz[size_t(i)], cudaMemcpyDefault, S(stream))) !=
+            cudaSuccess)
+          return cuda_fail(p, e);
+    }
+    return ELLM_OK;
+  }
   const int32_t* dd;
   both.push_back(0);  // the copy kernel's work-claim counter
   int rc = upload_ints(p, both, S(stream), &dd, nullptr);
@@ -1202,9 +1229,7 @@ int ellm_offload_layer(ellm_pool* p, int32_t layer, int32_t n, const int32_t* id
   uint8_t* hdev = nullptr;
   if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&hdev), p->host_slots, 0)) != cudaSuccess)
     return cuda_fail(p, e);
-  // layer l's K and V slabs of all local heads: [2][Hkv][T][d] bf16, contiguous in the chunk
-  const int64_t seg = int64_t(4) * p->cfg.n_heads_kv * p->T * p->cfg.head_dim;
-  if ((e = launch_chunk_copy(hdev, dd + n, static_cast<uint8_t*>(ellm_vtensor_base(p->vt)), dd, n, p->chunk_bytes,
+  if ((e = launch_chunk_copy(hdev, dd + n, pool, dd, n, p->chunk_bytes,
                              host_copy_grid(p), work_word(dd, 2 * n), S(stream), int64_t(layer) * seg, seg,
                              p->ash.rot, p->ash.slab, true, false)) != cudaSuccess)
     return cuda_fail(p, e);

@@ -38,17 +38,21 @@ def test_offload_metadata_matches_oracle_deflate():
 
 
 @pytest.mark.gpu
-def test_offload_layerwise_bytes_overlapped_with_appends():
+@pytest.mark.parametrize("mode,rotate", [(0, "0"), (1, "0"), (0, "1"), (1, "1")])
+def test_offload_layerwise_bytes_overlapped_with_appends(mode, rotate, monkeypatch):
     """Prefill request 1 layer by layer on the compute stream while each finished layer is
     offloaded on a second stream (event per layer); after commit the host slots hold exactly
-    what the oracle's deflate holds."""
+    what the oracle's deflate holds. SM copy kernel (mode 0) or copy engines (mode 1), canonical
+    or rotated slabs (request 1's chunks sit in the second rotation group)."""
     import torch
     from inputs import gen
     from tests.twin import Twin, bits_to_torch
+    monkeypatch.setenv("ELLM_ROTATE", rotate)
     L, Hq, Hkv, d, T = 4, 32, 8, 128, 16
-    t = Twin(L, Hq, Hkv, d, T, 64, 64, 2, 32, 32, seed=17)
-    assert t.reserve([0, 1], [100, 300]) == 0
-    t.append_all_layers([0], [100])
+    t = Twin(L, Hq, Hkv, d, T, 64, 64, 2, 40, 32, seed=17)
+    t.p.set_swap_mode(mode)
+    assert t.reserve([0, 1], [600, 300]) == 0
+    t.append_all_layers([0], [600])
     ids = t.p.table(1)[0].tolist()
     rc, slots = t.p.offload_begin(ids)
     assert rc == 0
