@@ -21,9 +21,12 @@ from inputs import workload as W  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--batch", type=int, default=32)
 ap.add_argument("--steps", type=int, default=6)
+ap.add_argument("--pad-gib", type=int, default=0, help="extra idle device allocation (GiB)")
+ap.add_argument("--only", default="", help="comma-separated variants (default: all)")
 a = ap.parse_args()
 wl = W.c2()
 wl.batch = a.batch
+pad = torch.empty(a.pad_gib << 30, dtype=torch.uint8, device="cuda") if a.pad_gib else None
 pool = W.make_pool(wl, 0)
 W.prefill(pool, wl)
 B, L = wl.batch, wl.n_layers
@@ -82,7 +85,8 @@ def timed(kind):
 
 step()
 base = timed(None)
-for kind in (None, "h2d", "d2h", "wr", "wr_fast"):
+kinds = [None] + ([k for k in a.only.split(",") if k] or ["h2d", "d2h", "wr", "wr_fast"])
+for kind in kinds:
     t = timed(kind)
     print(json.dumps({"variant": kind or "alone", "batch": B, "kv_gib": round(B * wl.context * 128 * 1024 / 2 ** 30, 1),
-                      "step_ms": round(t, 3), "slowdown": round(t / base, 3)}), flush=True)
+                      "pad_gib": a.pad_gib, "step_ms": round(t, 3), "slowdown": round(t / base, 3)}), flush=True)
