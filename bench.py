@@ -43,7 +43,7 @@ def parse():
                          "c5: 256-request prefill/decode churn with offload, compaction, shrink/grow")
     ap.add_argument("--swap-every", type=int, default=48,
                     help="c3: decode steps per offload/fetch round")
-    ap.add_argument("--swap-mode", choices=["sm", "ce", "mixed"], default="ce",
+    ap.add_argument("--swap-mode", choices=["sm", "ce", "mixed", "staged"], default="ce",
                     help="c3: swap with the SM copy kernels, the DMA copy engines, or copy engines for "
                          "swap-out and SM kernels for swap-in (mixed)")
     ap.add_argument("--resident", type=int, default=0,
@@ -734,7 +734,7 @@ def run_c3(args):
     cs = torch.cuda.current_stream()
     sp = cs.cuda_stream
     out_mode = 0 if args.swap_mode == "sm" else 1
-    in_mode = 1 if args.swap_mode == "ce" else 0
+    in_mode = {"ce": 1, "staged": 2}.get(args.swap_mode, 0)
     pool.set_swap_mode(out_mode)
     # placement: requests R+1.. are prefilled through the pool and offloaded; 0..R stay
     host_q = []

@@ -337,8 +337,11 @@ int ellm_gather_wait(ellm_pool* pool, int32_t layer, void* stream);
 /* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream): host <-> window copies. */
 int ellm_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
 
-/* Swap engine selection: 0 = SM copy kernels (default), 1 = DMA copy engines
- * (cudaMemcpyAsync per chunk). Both are exact byte copies. */
+/* Swap engine selection: 0 = SM copy kernels (default), 1 = DMA copy engines (one
+ * cudaMemcpyBatchAsync per call), 2 = as 1 for deflate / offload, and a staged inflate: the
+ * host link writes 256 MiB batches into a device staging buffer outside the KV pool, then an SM
+ * copy moves them into the chunks (inbound PCIe writes slow a concurrent decode more than
+ * device-side writes, DESIGN.md §5 C3). All are exact byte copies. INVALID_ARG outside 0..2. */
 int ellm_set_swap_mode(ellm_pool* pool, int32_t mode);
 
 /* ---- introspection (parity tests) --------------------------------------------------- */

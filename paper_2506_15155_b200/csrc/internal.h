@@ -251,7 +251,10 @@ struct ellm_pool {
   ellm::AttnShape ash{};
   int num_sms = 0;
   ellm::StagingRing ring;
-  int swap_mode = 0;
+  int swap_mode = 0;                 // 0 SM copy kernel, 1 copy engines, 2 staged inflate
+  uint8_t* d_stage = nullptr;        // swap_mode 2: device staging buffer for inflate (256 MiB)
+  cudaEvent_t stage_ev = nullptr;    // last use of the staging buffer
+  cudaStream_t stage_stream = nullptr;
   std::vector<ellm::TableUpdate> pending_updates;
 
   // attention descriptor cache

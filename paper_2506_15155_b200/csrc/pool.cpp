@@ -553,6 +553,8 @@ int ellm_pool_destroy(ellm_pool* p) {
     for (auto& fe : p->free_events)
       if (fe.ev) cudaEventDestroy(fe.ev);
     if (p->d_table) cudaFree(p->d_table);
+    if (p->d_stage) cudaFree(p->d_stage);
+    if (p->stage_ev) cudaEventDestroy(p->stage_ev);
     if (p->d_part) cudaFree(p->d_part);
     if (p->d_part_ml) cudaFree(p->d_part_ml);
     if (p->d_arrivals) cudaFree(p->d_arrivals);
@@ -604,7 +606,7 @@ void* ellm_pool_base(const ellm_pool* p) { return p && p->vt ? ellm_vtensor_base
 void* ellm_pool_host_base(const ellm_pool* p) { return p ? p->host_slots : nullptr; }
 
 int ellm_set_swap_mode(ellm_pool* p, int32_t mode) {
-  if (!p || (mode != 0 && mode != 1)) return ELLM_ERR_INVALID_ARG;
+  if (!p || mode < 0 || mode > 2) return ELLM_ERR_INVALID_ARG;
   p->swap_mode = mode;
   return ELLM_OK;
 }
@@ -1073,7 +1075,7 @@ int ellm_deflate(ellm_pool* p, int32_t n, const int32_t* ids, int32_t* slots_out
   for (int32_t h : dst)  // a slot last read by an inflate on another stream
     if ((e = wait_freed(p, p->slot_ev, h, S(stream))) != cudaSuccess) return cuda_fail(p, e);
   uint8_t* pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
-  if (p->swap_mode == 1) {
+  if (p->swap_mode >= 1) {
     if ((e = ce_copy(p->host_slots, dst, pool, src, p->chunk_bytes, S(stream), p->ash.rot, p->ash.slab, 1)) !=
         cudaSuccess)
       return cuda_fail(p, e);
@@ -1132,6 +1134,40 @@ int ellm_inflate(ellm_pool* p, int32_t n, const int32_t* slots, int32_t* ids_out
     if ((e = ce_copy(pool, dst, p->host_slots, src, p->chunk_bytes, S(stream), p->ash.rot, p->ash.slab, 2)) !=
         cudaSuccess)
       return cuda_fail(p, e);
+  } else if (p->swap_mode == 2) {
+    // staged: the host link writes into a device staging buffer outside the KV pool (copy
+    // engines), then an SM copy moves each batch into its chunks — inbound PCIe writes into the
+    // pool's VA slow a concurrent decode far more than device-side writes do (DESIGN.md §5 C3)
+    const int64_t S_chunks = std::max<int64_t>(1, (int64_t(256) << 20) / p->chunk_bytes);
+    if (!p->d_stage) {
+      if ((e = cudaMalloc(reinterpret_cast<void**>(&p->d_stage), size_t(S_chunks * p->chunk_bytes))) != cudaSuccess)
+        return cuda_fail(p, e);
+      if ((e = cudaEventCreateWithFlags(&p->stage_ev, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(p, e);
+    }
+    if (p->stage_stream && p->stage_stream != S(stream) &&
+        (e = cudaStreamWaitEvent(S(stream), p->stage_ev, 0)) != cudaSuccess)
+      return cuda_fail(p, e);
+    for (int32_t b0 = 0; b0 < n; b0 += int32_t(S_chunks)) {
+      const int32_t k = int32_t(std::min<int64_t>(S_chunks, n - b0));
+      std::vector<int32_t> sidx(static_cast<size_t>(k));
+      std::vector<int32_t> hs(src.begin() + b0, src.begin() + b0 + k);
+      for (int32_t i = 0; i < k; ++i) sidx[size_t(i)] = i;
+      if ((e = ce_copy(p->d_stage, sidx, p->host_slots, hs, p->chunk_bytes, S(stream))) != cudaSuccess)
+        return cuda_fail(p, e);
+      std::vector<int32_t> both(sidx);
+      both.insert(both.end(), dst.begin() + b0, dst.begin() + b0 + k);
+      both.push_back(0);  // the copy kernel's work-claim counter
+      const int32_t* dd;
+      int rc = upload_ints(p, both, S(stream), &dd, nullptr);
+      if (rc) return rc;
+      if ((e = launch_chunk_copy(pool, dd + k, p->d_stage, dd, k, p->chunk_bytes, 2 * p->num_sms,
+                                 work_word(dd, 2 * k), S(stream), 0, -1, p->ash.rot, p->ash.slab, false, true)) !=
+          cudaSuccess)
+        return cuda_fail(p, e);
+      ++p->launches;
+    }
+    if ((e = cudaEventRecord(p->stage_ev, S(stream))) != cudaSuccess) return cuda_fail(p, e);
+    p->stage_stream = S(stream);
   } else {
     std::vector<int32_t> both(src);
     both.insert(both.end(), dst.begin(), dst.end());
@@ -1198,7 +1234,7 @@ int ellm_offload_layer(ellm_pool* p, int32_t layer, int32_t n, const int32_t* id
   // layer l's K and V slabs of all local heads: [2][Hkv][T][d] bf16, contiguous in the chunk
   const int64_t seg = int64_t(4) * p->cfg.n_heads_kv * p->T * p->cfg.head_dim;
   uint8_t* pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
-  if (p->swap_mode == 1) {  // copy engines (no SMs taken from the prefill compute): one batch
+  if (p->swap_mode >= 1) {  // copy engines (no SMs taken from the prefill compute): one batch
     const size_t nn = static_cast<size_t>(n);
     std::vector<void*> d(nn), src(nn);
     std::vector<size_t> sz(nn, static_cast<size_t>(seg));

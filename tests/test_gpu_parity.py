@@ -145,7 +145,7 @@ def test_elastic_ops_bytes_and_attention():
             t.attention(l, resident)
 
 
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1, 2])
 def test_swap_modes_roundtrip(mode):
     t = Twin(2, 32, 8, 128, 16, 40, 40, 3, 12, 40, seed=2)
     t.p.set_swap_mode(mode)
