@@ -166,7 +166,8 @@ int ellm_kv_append(ellm_pool* pool, int32_t layer, int32_t n, const int32_t* req
  * KV read through the chunk table): for each listed request i (duplicates allowed) and
  * q-head h, out[i][h] = sum_j softmax_j(scale * q[i][h].k_j) v_j over j < len, with kv-head
  * h / (Hq/Hkv). q: device [n, Hq, d] bf16; out: device [n, Hq, d] bf16 (fp32 accumulate,
- * RNE). len == 0 -> INVALID_ARG; any chunk of the request in a host slot -> NOT_RESIDENT. */
+ * RNE). n > max_requests -> OUT_OF_RANGE (the per-call device state is sized by it); len == 0
+ * -> INVALID_ARG; any chunk of the request in a host slot -> NOT_RESIDENT. */
 int ellm_paged_decode_attention(ellm_pool* pool, int32_t layer, int32_t n, const int32_t* req_ids,
                                 const void* q, void* out, float softmax_scale, void* stream);
 
@@ -215,10 +216,13 @@ int ellm_inflate(ellm_pool* pool, int32_t n, const int32_t* host_slots, int32_t*
  * offload_layer: copy layer `layer`'s K/V slabs (2*Hkv*T*d*2 contiguous bytes per chunk) of the
  *   listed chunks to their reserved slots on `stream` — call it right after that layer's
  *   kv_append so the copy overlaps the following layers. The copy runs on the SM copy kernel,
- *   or as one cudaMemcpyBatchAsync on the DMA copy engines when ellm_set_swap_mode(1) (no SMs
- *   taken from the compute it overlaps). Chunk not being offloaded -> NOT_MAPPED. Appends into
- *   an offloading chunk after its layer was copied are not carried.
- * offload_commit: every layer of every listed chunk copied (else INVALID_ARG): repoint the
+ *   or on the DMA copy engines when ellm_set_swap_mode(1) (no SMs taken from the compute it
+ *   overlaps): one cudaMemcpy2DAsync per run of chunks whose ids and slots are both evenly
+ *   spaced, else one cudaMemcpyAsync per slab. Chunk not being offloaded -> NOT_MAPPED. Appends
+ *   into an offloading chunk after its layer was copied are not carried. A layer counts as
+ *   copied only once its copy was enqueued without error.
+ * offload_commit: every layer 0..L-1 of every listed chunk copied (a per-chunk layer bitset;
+ *   repeating one layer does not count for another; else INVALID_ARG): repoint the
  *   table entries to the slots and free the chunks — the same end state (tables, slots, bytes)
  *   as ellm_deflate of the same list. */
 int ellm_offload_begin(ellm_pool* pool, int32_t n, const int32_t* chunk_ids, int32_t* host_slots_out);
@@ -338,7 +342,8 @@ int ellm_gather_wait(ellm_pool* pool, int32_t layer, void* stream);
 int ellm_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
 
 /* Swap engine selection: 0 = SM copy kernels (default), 1 = DMA copy engines (one
- * cudaMemcpyBatchAsync per call), 2 = as 1 for deflate / offload, and a staged inflate: the
+ * cudaMemcpyAsync per maximal contiguous run of the chunk list, one cudaMemcpy2DAsync per maximal
+ * evenly strided run), 2 = as 1 for deflate / offload, and a staged inflate: the
  * host link writes 256 MiB batches into a device staging buffer outside the KV pool, then an SM
  * copy moves them into the chunks (inbound PCIe writes slow a concurrent decode more than
  * device-side writes, DESIGN.md §5 C3). All are exact byte copies. INVALID_ARG outside 0..2. */

@@ -283,7 +283,9 @@ struct ellm_pool {
   std::vector<int32_t> free_event_pool;          // indices of unreferenced events
   std::vector<int32_t> chunk_ev, slot_ev;        // per chunk / host slot: event index or -1
   // layer-wise offload in progress (ellm_offload_*): reserved slot and layers copied, per chunk
-  std::vector<int32_t> off_slot, off_layers;
+  std::vector<int32_t> off_slot;
+  std::vector<uint64_t> off_layers;  // per chunk: bitset of layers copied by offload_layer (off_words words)
+  int64_t off_words = 1;
 
   // f1: VMM work off the caller's critical path. A worker thread keeps
   // the `premap_units` lowest all-ACT units mapped ahead of pool_grow (speculative pre-mapping)

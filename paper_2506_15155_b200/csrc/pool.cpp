@@ -88,48 +88,68 @@ void free_host(ellm_pool* p, int64_t h) {
 
 cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// Copy-engine path of deflate / inflate: dst_base[dst[i]] <- src_base[src[i]], chunk_bytes each,
-// as ONE cudaMemcpyBatchAsync (host cost independent of the chunk count; copies prefer to
-// overlap with compute). Falls back to one cudaMemcpyAsync per chunk if the batch API fails.
+// Copy-engine (DMA) copies. Each piece is (dst, src, bytes); pieces are issued as one
+// cudaMemcpyAsync per maximal contiguous run (both sides advance by the piece size) or one
+// cudaMemcpy2DAsync per maximal strided run (equal sizes, constant dst and src strides: e.g.
+// consecutive chunk ids whose host slots are consecutive, or one layer slab of each). The host
+// cost is then per run, not per chunk; the copies are exact byte copies either way.
+struct CopyPiece {
+  uint8_t* d;
+  const uint8_t* s;
+  int64_t n;
+};
+cudaError_t issue_copies(const std::vector<CopyPiece>& pc, cudaStream_t stream) {
+  size_t i = 0;
+  while (i < pc.size()) {
+    const CopyPiece& a = pc[i];
+    size_t j = i + 1;
+    if (j < pc.size() && pc[j].n == a.n && pc[j].d - a.d >= a.n && pc[j].s - a.s >= a.n) {
+      const int64_t dp = pc[j].d - a.d, sp = pc[j].s - a.s;
+      while (j < pc.size() && pc[j].n == a.n && pc[j].d - pc[j - 1].d == dp && pc[j].s - pc[j - 1].s == sp) ++j;
+      const size_t rows = j - i;
+      cudaError_t e;
+      if (dp == a.n && sp == a.n)
+        e = cudaMemcpyAsync(a.d, a.s, size_t(a.n) * rows, cudaMemcpyDefault, stream);
+      else
+        e = cudaMemcpy2DAsync(a.d, size_t(dp), a.s, size_t(sp), size_t(a.n), rows, cudaMemcpyDefault, stream);
+      if (e != cudaSuccess) return e;
+    } else {
+      cudaError_t e = cudaMemcpyAsync(a.d, a.s, size_t(a.n), cudaMemcpyDefault, stream);
+      if (e != cudaSuccess) return e;
+    }
+    i = j;
+  }
+  return cudaSuccess;
+}
+
+// Copy-engine path of deflate / inflate: dst_base[dst[i]] <- src_base[src[i]], chunk_bytes each.
 // With rotated slabs (rot = L) the pool side of chunk c holds canonical layers [0, L-r) at slots
-// [r, L) and [L-r, L) at [0, r), r = slab_shift(c): two copies per chunk (dev_side: 1 = src,
-// 2 = dst).
+// [r, L) and [L-r, L) at [0, r), r = slab_shift(c): two pieces per chunk (dev_side: 1 = src,
+// 2 = dst). The pieces are listed piece-major (all first pieces, then all second pieces) so that
+// chunks of one rotation group with consecutive ids and slots form one strided run each.
 cudaError_t ce_copy(uint8_t* dst_base, const std::vector<int32_t>& dst, const uint8_t* src_base,
                     const std::vector<int32_t>& src, int64_t chunk_bytes, cudaStream_t stream,
                     int32_t rot = 0, int64_t slab = 0, int dev_side = 0) {
-  std::vector<void*> d, s;
-  std::vector<size_t> sz;
-  for (size_t i = 0; i < dst.size(); ++i) {
-    uint8_t* dc = dst_base + int64_t(dst[i]) * chunk_bytes;
-    uint8_t* sc = const_cast<uint8_t*>(src_base) + int64_t(src[i]) * chunk_bytes;
-    const int64_t r = slab_shift(dev_side == 1 ? src[i] : dst[i], rot);
-    if (r == 0) {
-      d.push_back(dc), s.push_back(sc), sz.push_back(size_t(chunk_bytes));
-      continue;
+  std::vector<CopyPiece> pc;
+  pc.reserve(dst.size());
+  for (int k = 0; k < 2; ++k)
+    for (size_t i = 0; i < dst.size(); ++i) {
+      uint8_t* dc = dst_base + int64_t(dst[i]) * chunk_bytes;
+      const uint8_t* sc = src_base + int64_t(src[i]) * chunk_bytes;
+      const int64_t r = slab_shift(dev_side == 1 ? src[i] : dst[i], rot);
+      if (r == 0) {
+        if (k == 0) pc.push_back({dc, sc, chunk_bytes});
+        continue;
+      }
+      // canonical layers [0, L-r) <-> device slots [r, L); layers [L-r, L) <-> slots [0, r)
+      const int64_t canon_off = k == 0 ? 0 : (rot - r) * slab, dev_off = k == 0 ? r * slab : 0;
+      const int64_t len = k == 0 ? (rot - r) * slab : r * slab;
+      if (dev_side == 1)
+        pc.push_back({dc + canon_off, sc + dev_off, len});
+      else
+        pc.push_back({dc + dev_off, sc + canon_off, len});
     }
-    uint8_t* canon = dev_side == 1 ? dc : sc;  // canonical side
-    uint8_t* dev = dev_side == 1 ? sc : dc;
-    uint8_t* a[2] = {canon, canon + (rot - r) * slab};          // layers [0, L-r), [L-r, L)
-    uint8_t* b[2] = {dev + r * slab, dev};                      // slots  [r, L),   [0, r)
-    const size_t len[2] = {size_t((rot - r) * slab), size_t(r * slab)};
-    for (int k = 0; k < 2; ++k) {
-      d.push_back(dev_side == 1 ? a[k] : b[k]);
-      s.push_back(dev_side == 1 ? b[k] : a[k]);
-      sz.push_back(len[k]);
-    }
-  }
-  const size_t n = d.size();
-  cudaMemcpyAttributes attr;
-  std::memset(&attr, 0, sizeof(attr));
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-  size_t attr_idx = 0, fail_idx = 0;
-  cudaError_t e = cudaMemcpyBatchAsync(d.data(), s.data(), sz.data(), n, &attr, &attr_idx, 1, &fail_idx, stream);
-  if (e == cudaSuccess) return e;
-  cudaGetLastError();
-  for (size_t i = 0; i < n; ++i)
-    if ((e = cudaMemcpyAsync(d[i], s[i], sz[i], cudaMemcpyDefault, stream)) != cudaSuccess) return e;
-  return cudaSuccess;
+  return issue_copies(pc, stream);
 }
 
 // ---- stream-ordered reuse of freed chunks / host slots (see ellm_pool::FreeEvent) ----------
@@ -418,7 +438,8 @@ int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out) {
   p->in_act.assign(size_t(c.max_chunks), 0);
   p->slot_ev.assign(size_t(c.host_slots), -1);
   p->off_slot.assign(size_t(c.max_chunks), -1);
-  p->off_layers.assign(size_t(c.max_chunks), 0);
+  p->off_words = (c.n_layers + 63) / 64;
+  p->off_layers.assign(size_t(c.max_chunks) * size_t(p->off_words), 0);
   p->table.assign(size_t(int64_t(c.max_requests) * c.max_chunks_per_request), UNMAPPED);
   p->len.assign(size_t(c.max_requests), 0);
   p->pending.assign(size_t(c.max_requests), 0);
@@ -702,6 +723,7 @@ int ellm_paged_decode_attention(ellm_pool* p, int32_t layer, int32_t n, const in
   if (!p || n < 0 || (n > 0 && !reqs)) return ELLM_ERR_INVALID_ARG;
   if (layer < 0 || layer >= p->cfg.n_layers) return ELLM_ERR_OUT_OF_RANGE;
   if (!check_reqs_range(p, n, reqs)) return ELLM_ERR_OUT_OF_RANGE;
+  if (n > p->cfg.max_requests) return ELLM_ERR_OUT_OF_RANGE;  // per-call device buffers hold max_requests
   for (int32_t i = 0; i < n; ++i)
     if (p->len[size_t(reqs[i])] == 0) return ELLM_ERR_INVALID_ARG;
   for (int32_t i = 0; i < n; ++i)
@@ -718,6 +740,7 @@ int ellm_decode_append_attention(ellm_pool* p, int32_t layer, int32_t n, const i
   if (!p || n < 0 || (n > 0 && !reqs)) return ELLM_ERR_INVALID_ARG;
   if (layer < 0 || layer >= p->cfg.n_layers) return ELLM_ERR_OUT_OF_RANGE;
   if (!check_reqs_range(p, n, reqs)) return ELLM_ERR_OUT_OF_RANGE;
+  if (n > p->cfg.max_requests) return ELLM_ERR_OUT_OF_RANGE;
   if (has_dup(n, reqs)) return ELLM_ERR_INVALID_ARG;
   for (int32_t i = 0; i < n; ++i)
     if (p->pending[size_t(reqs[i])] != 1) return ELLM_ERR_INVALID_ARG;
@@ -810,6 +833,7 @@ int ellm_attention_gather(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
   if (!p || n < 0 || (n > 0 && !reqs)) return ELLM_ERR_INVALID_ARG;
   if (layer < 0 || layer >= p->cfg.n_layers) return ELLM_ERR_OUT_OF_RANGE;
   if (!check_reqs_range(p, n, reqs)) return ELLM_ERR_OUT_OF_RANGE;
+  if (n > p->cfg.max_requests) return ELLM_ERR_OUT_OF_RANGE;  // per-call device buffers hold max_requests
   if (p->g_world == 0 || out_offset < 0 || out_offset % 16) return ELLM_ERR_INVALID_ARG;
   const int64_t rows_bytes = int64_t(n) * p->g_hq_out * p->cfg.head_dim * 2;
   if (out_offset + rows_bytes > p->g_win_bytes - ELLM_GATHER_DATA_OFFSET) return ELLM_ERR_OUT_OF_RANGE;
@@ -1207,7 +1231,7 @@ int ellm_offload_begin(ellm_pool* p, int32_t n, const int32_t* ids, int32_t* slo
     p->slot_req[size_t(h)] = p->chunk_req[size_t(c)];
     p->slot_idx[size_t(h)] = p->chunk_idx[size_t(c)];
     p->off_slot[size_t(c)] = int32_t(h);
-    p->off_layers[size_t(c)] = 0;
+    std::fill_n(p->off_layers.begin() + c * p->off_words, p->off_words, uint64_t(0));
     slots_out[i] = int32_t(h);
   }
   return ELLM_OK;
@@ -1225,37 +1249,31 @@ int ellm_offload_layer(ellm_pool* p, int32_t layer, int32_t n, const int32_t* id
   for (int32_t i = 0; i < n; ++i) {
     both[size_t(i)] = ids[i];
     both[size_t(n + i)] = p->off_slot[size_t(ids[i])];
-    ++p->off_layers[size_t(ids[i])];
   }
-  if (!p->has_dev || n == 0) return ELLM_OK;
+  // layer `layer` of each listed chunk is marked copied only once its copy is enqueued
+  auto mark_copied = [&]() {
+    for (int32_t i = 0; i < n; ++i)
+      p->off_layers[size_t(int64_t(ids[i]) * p->off_words + layer / 64)] |= uint64_t(1) << (layer % 64);
+  };
+  if (!p->has_dev || n == 0) {
+    mark_copied();
+    return ELLM_OK;
+  }
   cudaError_t e;
   for (int32_t i = 0; i < n; ++i)  // the reserved slot may have been read by an inflate elsewhere
     if ((e = wait_freed(p, p->slot_ev, both[size_t(n + i)], S(stream))) != cudaSuccess) return cuda_fail(p, e);
   // layer l's K and V slabs of all local heads: [2][Hkv][T][d] bf16, contiguous in the chunk
   const int64_t seg = int64_t(4) * p->cfg.n_heads_kv * p->T * p->cfg.head_dim;
   uint8_t* pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
-  if (p->swap_mode >= 1) {  // copy engines (no SMs taken from the prefill compute): one batch
-    const size_t nn = static_cast<size_t>(n);
-    std::vector<void*> d(nn), src(nn);
-    std::vector<size_t> sz(nn, static_cast<size_t>(seg));
+  if (p->swap_mode >= 1) {  // copy engines (no SMs taken from the prefill compute)
+    std::vector<CopyPiece> pc(static_cast<size_t>(n));
     for (int32_t i = 0; i < n; ++i) {
       const int64_t c = ids[i], h = both[size_t(n + i)];
-      src[size_t(i)] = pool + c * p->chunk_bytes + int64_t(slab_slot(c, layer, p->ash.rot)) * seg;
-      d[size_t(i)] = p->host_slots + h * p->chunk_bytes + int64_t(layer) * seg;
+      pc[size_t(i)] = {p->host_slots + h * p->chunk_bytes + int64_t(layer) * seg,
+                       pool + c * p->chunk_bytes + int64_t(slab_slot(c, layer, p->ash.rot)) * seg, seg};
     }
-    cudaMemcpyAttributes attr;
-    std::memset(&attr, 0, sizeof(attr));
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-    size_t attr_idx = 0, fail_idx = 0;
-    e = cudaMemcpyBatchAsync(d.data(), src.data(), sz.data(), size_t(n), &attr, &attr_idx, 1, &fail_idx, S(stream));
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      for (int32_t i = 0; i < n; ++i)
-        if ((e = cudaMemcpyAsync(d[size_t(i)], src[size_t(i)], sz[size_t(i)], cudaMemcpyDefault, S(stream))) !=
-            cudaSuccess)
-          return cuda_fail(p, e);
-    }
+    if ((e = issue_copies(pc, S(stream))) != cudaSuccess) return cuda_fail(p, e);
+    mark_copied();
     return ELLM_OK;
   }
   const int32_t* dd;
@@ -1270,6 +1288,7 @@ int ellm_offload_layer(ellm_pool* p, int32_t layer, int32_t n, const int32_t* id
                              p->ash.rot, p->ash.slab, true, false)) != cudaSuccess)
     return cuda_fail(p, e);
   ++p->launches;
+  mark_copied();
   return p->ring.commit(S(stream));
 }
 
@@ -1281,7 +1300,9 @@ int ellm_offload_commit(ellm_pool* p, int32_t n, const int32_t* ids, void* strea
   for (int32_t i = 0; i < n; ++i)
     if (p->off_slot[size_t(ids[i])] < 0) return ELLM_ERR_NOT_MAPPED;
   for (int32_t i = 0; i < n; ++i)
-    if (p->off_layers[size_t(ids[i])] < p->cfg.n_layers) return ELLM_ERR_INVALID_ARG;
+    for (int32_t l = 0; l < p->cfg.n_layers; ++l)
+      if (!((p->off_layers[size_t(int64_t(ids[i]) * p->off_words + l / 64)] >> (l % 64)) & 1))
+        return ELLM_ERR_INVALID_ARG;  // a layer of this chunk was never copied
   const int32_t ev = p->has_dev && n > 0 ? record_free_event(p, S(stream)) : -1;
   if (p->has_dev && n > 0 && ev < 0) return ELLM_ERR_CUDA;
   for (int32_t i = 0; i < n; ++i) {
