@@ -313,14 +313,20 @@ def main():
     for s in range(n_ring):
         inputs.append(W.decode_inputs(wl, s, lens + s))
     out = torch.empty((L, B, wl.hq_local, wl.head_dim), dtype=torch.bfloat16, device="cuda")
-    p2p = world > 1 and args.gather == "p2p"
+    # --emulate-shard N issues rank 0's real N>1 call sequence (attention_gather + folded waits)
+    # into a world-1 window: the per-GPU step minus the N-1 remote copies of each output row
+    emulate = args.emulate_shard > 1
+    p2p = (world > 1 or emulate) and args.gather == "p2p"
     gath = torch.empty((L, world, B, wl.hq_local, wl.head_dim), dtype=torch.bfloat16, device="cuda") \
         if world > 1 and not p2p else None
     pg = None
     if p2p:  # a10 fused: every rank's attention stores its heads' rows into all ranks' windows
         from paper_2506_15155_b200 import shard
-        pg = shard.PeerGather(pool, world, rank, wl.n_heads_q, L, B, wl.head_dim, device=local)
-        dist.barrier()
+        if emulate:
+            pg = shard.PeerGather(pool, 1, 0, wl.hq_local, L, B, wl.head_dim, device=local)
+        else:
+            pg = shard.PeerGather(pool, world, rank, wl.n_heads_q, L, B, wl.head_dim, device=local)
+            dist.barrier()
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
     attn_ev, app_ev, reserve_s = [], [], []
@@ -332,16 +338,21 @@ def main():
             reserve_s.append(time.perf_counter() - t0)
         if rc:
             raise ellm.EllmError(rc, "reserve")
-        # world == 1, fused: one event pair around the L back-to-back launches (an event between
-        # two launches would keep the next from overlapping the previous one's tail, PDL), so the
-        # per-launch time is the span / L; otherwise one pair per launch
-        span = fused and pg is None and gath is None
+        # fused: one event pair around the L back-to-back launches (an event between two
+        # launches would keep the next from overlapping the previous one's tail, PDL), so the
+        # per-launch time is the span / L; otherwise one pair per launch. With the p2p gather the
+        # span includes the step's final gather_wait kernel.
+        span = fused and gath is None
         for l in range(L):
             if fused:  # kv_append + attention + split-K merge in one launch per layer
                 if record and (not span or l == 0):
                     e0 = torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
                 if pg is not None:  # ... + the head gather (a10) in the same launch
+                    if l > 0:  # Q(l) needs every rank's rows of layer l-1: waited for inside
+                        rc = pool.gather_wait_next(l - 1)  # this launch, after its first K/V TMAs
+                        if rc:
+                            raise ellm.EllmError(rc, "gather_wait_next")
                     rc = pool.attention_gather(l, reqs, q[l], pg.offset(l), scale, k[l], v[l], sp)
                 else:
                     rc = pool.decode_append_attention(l, reqs, k[l], v[l], q[l], out[l], scale, sp)
@@ -364,15 +375,15 @@ def main():
                     rc = pool.attention(l, reqs, q[l], out[l], scale, sp)
                 if rc:
                     raise ellm.EllmError(rc, "attention")
+            if pg is not None and (l == L - 1 or not fused):  # the step's result: every rank's rows
+                rc = pool.gather_wait(l, sp)
+                if rc:
+                    raise ellm.EllmError(rc, "gather_wait")
             if record and (not span or l == L - 1):
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(stream)
                 attn_ev.append((e0, e1, L if span else 1))
-            if pg is not None:  # the layer's consumer waits for every rank's rows
-                rc = pool.gather_wait(l, sp)
-                if rc:
-                    raise ellm.EllmError(rc, "gather_wait")
-            elif gath is not None:
+            if gath is not None:
                 dist.all_gather_into_tensor(gath[l], out[l])
 
     def barrier():
@@ -674,10 +685,15 @@ def main():
                 "data": "synthetic (seeded counter-based generator, 3 needles per request/layer/kv-head)",
                 "config": {**workload_config(wl, world),
                            **({"parallelism": f"rank 0 of a kv-head shard x{args.emulate_shard}, run alone on "
-                                              "1 GPU (no gather): per-GPU rate at that geometry"}
+                                              "1 GPU: per-GPU rate at that geometry, with rank 0's N>1 call "
+                                              "sequence (gather into a world-1 window: the N-1 remote row "
+                                              "copies over NVLink are not issued)"}
                               if args.emulate_shard > 1 else {}),
-                           **({"gather": "fused attention epilogue, P2P stores into every rank's window"
-                               if pg is not None else "NCCL all_gather_into_tensor per layer"} if world > 1 else {})},
+                           **({"gather": "fused attention epilogue, P2P stores into every rank's window; "
+                                         "layer l's wait folded into layer l+1's launch, gather_wait after "
+                                         "the last layer"
+                               if pg is not None else "NCCL all_gather_into_tensor per layer"}
+                              if world > 1 or args.emulate_shard > 1 else {})},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk.summary(),
                 "attention_gbs": round(achieved, 1), "attention_frac_of_peak": roof["frac"], "swap": swap,

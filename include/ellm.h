@@ -166,8 +166,9 @@ int ellm_kv_append(ellm_pool* pool, int32_t layer, int32_t n, const int32_t* req
  * KV read through the chunk table): for each listed request i (duplicates allowed) and
  * q-head h, out[i][h] = sum_j softmax_j(scale * q[i][h].k_j) v_j over j < len, with kv-head
  * h / (Hq/Hkv). q: device [n, Hq, d] bf16; out: device [n, Hq, d] bf16 (fp32 accumulate,
- * RNE). n > max_requests -> OUT_OF_RANGE (the per-call device state is sized by it); len == 0
- * -> INVALID_ARG; any chunk of the request in a host slot -> NOT_RESIDENT. */
+ * RNE). A list longer than max_requests (repeated ids) grows the split-K state once, which
+ * synchronises the device. len == 0 -> INVALID_ARG; any chunk of the request in a host slot ->
+ * NOT_RESIDENT. */
 int ellm_paged_decode_attention(ellm_pool* pool, int32_t layer, int32_t n, const int32_t* req_ids,
                                 const void* q, void* out, float softmax_scale, void* stream);
 
@@ -338,6 +339,17 @@ int ellm_attention_gather(ellm_pool* pool, int32_t layer, int32_t n, const int32
                           const void* k_new, const void* v_new, const void* q, int64_t out_offset,
                           float softmax_scale, void* stream);
 int ellm_gather_wait(ellm_pool* pool, int32_t layer, void* stream);
+/* gather_wait_next: the same ordering as gather_wait(layer), folded into the NEXT attention
+ * launch of this pool (paged_decode_attention, decode_append_attention or attention_gather, on
+ * the stream the caller would have passed to gather_wait): that launch's producer warp streams
+ * its first K/V tiles, then spins (acquire, system scope, bounded like gather_wait) until the
+ * flag of `layer` reaches the target fixed by this call, and only then stages Q or writes. This
+ * models Q(l+1) depending on the gathered rows of layer l without a wait kernel between two
+ * attention launches, so they still overlap (launch overlap / PDL). Without a following attention
+ * launch nothing waits: call gather_wait instead. Requires that the peers' launches progress
+ * independently of this launch (one GPU per rank, or ranks sharing one stream): a spinning CTA
+ * holds its SM. Errors as gather_wait; no stream argument. */
+int ellm_gather_wait_next(ellm_pool* pool, int32_t layer);
 /* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream): host <-> window copies. */
 int ellm_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
 

@@ -22,6 +22,8 @@
 //  * Each warp writes an fp32 partial (m, l, o) per (CTA, request); the last CTA to finish a
 //    request (per-request arrival counter) merges its partials with the log-sum-exp rule and
 //    writes the bf16 output, so one launch does rows a4 and a5.
+#include <cstdio>
+
 #include <cuda_bf16.h>
 
 #include "internal.h"
@@ -157,6 +159,12 @@ struct Params {
   __nv_bfloat16* gout[kMaxPeers];
   uint32_t* gflag[kMaxPeers];
   int32_t n_peer, Hq_out, q_off;
+  // a10 folded wait (ellm_gather_wait_next): the previous layer's gather must be complete in
+  // this rank's window before this launch stages Q or writes (Q of layer l+1 is computed from
+  // the gathered rows of layer l in a model); nullptr = no wait
+  const uint32_t* wait_flag;
+  uint32_t wait_target;
+  unsigned long long wait_timeout_ns;
 };
 constexpr int kFirst = 1, kLast = 2, kDone = 4;  // stage metadata flags
 
@@ -242,7 +250,26 @@ __device__ __forceinline__ void merge_request(const Params& p, int vr, int rows,
   }
 }
 
-// largest vr with cum[vr] <= t
+// One thread spins (acquire, system scope) until *flag - target >= 0 (wrapping counters);
+// bounded: after timeout_ns it reports and traps so a lost peer fails the stream loudly.
+__device__ __noinline__ void gather_flag_spin(const uint32_t* flag, uint32_t target,
+                                              unsigned long long timeout_ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (int32_t(v - target) >= 0) return;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) {
+      printf("ellm attention: folded gather wait, flag %u < target %u after %llu ns\n", v, target,
+             static_cast<unsigned long long>(t - t0));
+      __trap();
+    }
+    __nanosleep(64);
+  }
+}
+
 // The largest vr with cum[vr] <= t (cum non-decreasing, cum[0] = 0 <= t), found by the whole
 // warp: each round the 32 lanes probe evenly spaced entries and the bracket shrinks 32x, so a
 // CTA's first lookup costs ceil(log32 n_vr) dependent loads instead of log2 n_vr (launch ramp).
@@ -353,6 +380,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto pdl_wait = [&]() {
       if (!waited) {
         asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (p.wait_flag != nullptr) {  // folded a10 wait: every rank's rows of the previous layer
+          if (lane == 0) gather_flag_spin(p.wait_flag, p.wait_target, p.wait_timeout_ns);
+          __syncwarp();
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // before any TMA of Q
+        }
         waited = true;
       }
     };
@@ -823,6 +855,9 @@ cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh,
     prm.gout[i] = static_cast<__nv_bfloat16*>(plan.gout[i]);
     prm.gflag[i] = plan.gflag[i];
   }
+  prm.wait_flag = plan.wait_flag;
+  prm.wait_target = plan.wait_target;
+  prm.wait_timeout_ns = plan.wait_timeout_ns;
   cudaError_t e;
   if (sh.D == 128) {
     switch (sh.HB) {

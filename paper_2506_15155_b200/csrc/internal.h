@@ -165,6 +165,11 @@ struct AttnPlan {
   void* gout[kMaxPeers] = {};
   uint32_t* gflag[kMaxPeers] = {};
   int32_t n_peer = 0, Hq_out = 0, q_off = 0;
+  // a10 folded gather wait (ellm_gather_wait_next): before staging Q or writing anything, the
+  // producer spins (acquire, system scope) until *wait_flag reaches wait_target; nullptr = none
+  const uint32_t* wait_flag = nullptr;
+  uint32_t wait_target = 0;
+  uint64_t wait_timeout_ns = 0;
   // programmatic dependent launch: this launch may start while the previous kernel on the
   // stream finishes (attention.cu: K/V streamed before griddepcontrol.wait, all else after)
   bool pdl = false;
@@ -247,6 +252,7 @@ struct ellm_pool {
   float* d_part_ml = nullptr;
   int32_t* d_arrivals = nullptr;     // per virtual request, for the fused split-K merge
   int64_t part_records = 0;
+  int64_t attn_cap = 0;              // list entries the split-K state above is sized for
   CUtensorMap tmap{};
   ellm::AttnShape ash{};
   int num_sms = 0;
@@ -326,6 +332,8 @@ struct ellm_pool {
   int64_t g_win_bytes = 0;
   std::vector<uint32_t> g_expect;
   uint64_t g_timeout_ns = 20000000000ull;
+  const uint32_t* g_wait_flag = nullptr;  // folded wait (ellm_gather_wait_next) for the next launch
+  uint32_t g_wait_target = 0;
 
   // programmatic dependent launch of attention (attention.cu; ellm_set_launch_overlap, ELLM_PDL)
   bool pdl = false;

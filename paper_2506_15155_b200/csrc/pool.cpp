@@ -398,6 +398,36 @@ const char* ellm_status_string(int s) {
 int ellm_last_cuda_error(const ellm_pool* p) { return p ? p->last_cuda_error : 0; }
 int64_t ellm_kernel_launches(const ellm_pool* p) { return p ? p->launches : 0; }
 
+// Split-K state of the attention launches, sized for calls of up to `reqs` list entries
+// (duplicates allowed, so a call may list more than max_requests): partial records
+// pid < (G + 2 n_vr + n_dyn) * nsub, each [HB*group][D] fp32 + (m, l), and one arrival counter
+// per virtual request (zero between launches). Grown on demand by attention_impl; growing
+// synchronises the device (in-flight launches use the old buffers).
+static int alloc_attn_state(ellm_pool* p, int64_t reqs) {
+  const AttnShape& a = p->ash;
+  const int64_t group = a.group;
+  if (p->d_part || p->d_part_ml || p->d_arrivals) {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(p, e);
+    cudaFree(p->d_part);
+    cudaFree(p->d_part_ml);
+    cudaFree(p->d_arrivals);
+    p->d_part = p->d_part_ml = nullptr;
+    p->d_arrivals = nullptr;
+  }
+  p->part_records = (int64_t(p->num_sms) + 2 * reqs * a.HG + kMaxDynUnits) * a.nsub;
+  cudaError_t e;
+  if ((e = cudaMalloc(reinterpret_cast<void**>(&p->d_part),
+                      size_t(p->part_records) * a.HB * group * a.D * 4)) != cudaSuccess ||
+      (e = cudaMalloc(reinterpret_cast<void**>(&p->d_part_ml),
+                      size_t(p->part_records) * a.HB * group * 2 * 4)) != cudaSuccess ||
+      (e = cudaMalloc(reinterpret_cast<void**>(&p->d_arrivals), size_t(reqs) * a.HG * 4)) != cudaSuccess ||
+      (e = cudaMemset(p->d_arrivals, 0, size_t(reqs) * a.HG * 4)) != cudaSuccess)
+    return cuda_fail(p, e);
+  p->attn_cap = reqs;
+  return ELLM_OK;
+}
+
 int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out) {
   if (!cfg || !out) return ELLM_ERR_INVALID_ARG;
   *out = nullptr;
@@ -528,16 +558,8 @@ int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out) {
   bool want_rot = (p->chunk_bytes & (p->chunk_bytes - 1)) != 0;
   if (const char* v = std::getenv("ELLM_ROTATE")) want_rot = std::atoi(v) != 0;
   a.rot = (can_rot && want_rot) ? c.n_layers : 0;
-  // split-K partial records: pid < (G + n_vr) * nsub, each [HB*group][D] fp32 + (m, l)
-  p->part_records = (int64_t(p->num_sms) + 2 * int64_t(c.max_requests) * a.HG + kMaxDynUnits) * a.nsub;
-  if ((e = cudaMalloc(reinterpret_cast<void**>(&p->d_part),
-                      size_t(p->part_records) * a.HB * group * a.D * 4)) != cudaSuccess ||
-      (e = cudaMalloc(reinterpret_cast<void**>(&p->d_part_ml),
-                      size_t(p->part_records) * a.HB * group * 2 * 4)) != cudaSuccess ||
-      (e = cudaMalloc(reinterpret_cast<void**>(&p->d_arrivals),
-                      size_t(c.max_requests) * a.HG * 4)) != cudaSuccess ||
-      (e = cudaMemset(p->d_arrivals, 0, size_t(c.max_requests) * a.HG * 4)) != cudaSuccess ||
-      (e = cudaMalloc(reinterpret_cast<void**>(&p->d_ticket), 8)) != cudaSuccess ||
+  if ((rc = alloc_attn_state(p, c.max_requests))) return fail(rc);
+  if ((e = cudaMalloc(reinterpret_cast<void**>(&p->d_ticket), 8)) != cudaSuccess ||
       (e = cudaMemset(p->d_ticket, 0, 8)) != cudaSuccess)
     return fail(cuda_fail(p, e));
   if ((rc = p->ring.init(size_t(1) << 20, 16))) return fail(rc);
@@ -723,7 +745,6 @@ int ellm_paged_decode_attention(ellm_pool* p, int32_t layer, int32_t n, const in
   if (!p || n < 0 || (n > 0 && !reqs)) return ELLM_ERR_INVALID_ARG;
   if (layer < 0 || layer >= p->cfg.n_layers) return ELLM_ERR_OUT_OF_RANGE;
   if (!check_reqs_range(p, n, reqs)) return ELLM_ERR_OUT_OF_RANGE;
-  if (n > p->cfg.max_requests) return ELLM_ERR_OUT_OF_RANGE;  // per-call device buffers hold max_requests
   for (int32_t i = 0; i < n; ++i)
     if (p->len[size_t(reqs[i])] == 0) return ELLM_ERR_INVALID_ARG;
   for (int32_t i = 0; i < n; ++i)
@@ -740,7 +761,6 @@ int ellm_decode_append_attention(ellm_pool* p, int32_t layer, int32_t n, const i
   if (!p || n < 0 || (n > 0 && !reqs)) return ELLM_ERR_INVALID_ARG;
   if (layer < 0 || layer >= p->cfg.n_layers) return ELLM_ERR_OUT_OF_RANGE;
   if (!check_reqs_range(p, n, reqs)) return ELLM_ERR_OUT_OF_RANGE;
-  if (n > p->cfg.max_requests) return ELLM_ERR_OUT_OF_RANGE;
   if (has_dup(n, reqs)) return ELLM_ERR_INVALID_ARG;
   for (int32_t i = 0; i < n; ++i)
     if (p->pending[size_t(reqs[i])] != 1) return ELLM_ERR_INVALID_ARG;
@@ -825,6 +845,7 @@ int ellm_gather_detach(ellm_pool* p) {
   p->g_world = 0;
   p->g_win.clear();
   p->g_expect.clear();
+  p->g_wait_flag = nullptr;
   return ELLM_OK;
 }
 
@@ -833,7 +854,6 @@ int ellm_attention_gather(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
   if (!p || n < 0 || (n > 0 && !reqs)) return ELLM_ERR_INVALID_ARG;
   if (layer < 0 || layer >= p->cfg.n_layers) return ELLM_ERR_OUT_OF_RANGE;
   if (!check_reqs_range(p, n, reqs)) return ELLM_ERR_OUT_OF_RANGE;
-  if (n > p->cfg.max_requests) return ELLM_ERR_OUT_OF_RANGE;  // per-call device buffers hold max_requests
   if (p->g_world == 0 || out_offset < 0 || out_offset % 16) return ELLM_ERR_INVALID_ARG;
   const int64_t rows_bytes = int64_t(n) * p->g_hq_out * p->cfg.head_dim * 2;
   if (out_offset + rows_bytes > p->g_win_bytes - ELLM_GATHER_DATA_OFFSET) return ELLM_ERR_OUT_OF_RANGE;
@@ -865,12 +885,29 @@ int ellm_gather_wait(ellm_pool* p, int32_t layer, void* stream) {
   return ELLM_OK;
 }
 
+// a10, folded: the next attention launch of this pool waits in its producer for `layer`'s gather
+// (the target the flag must reach is fixed now), so no wait kernel sits between two attention
+// launches and programmatic dependent launch stays on at N > 1.
+int ellm_gather_wait_next(ellm_pool* p, int32_t layer) {
+  if (!p) return ELLM_ERR_INVALID_ARG;
+  if (layer < 0 || layer >= p->cfg.n_layers) return ELLM_ERR_OUT_OF_RANGE;
+  if (p->g_world == 0) return ELLM_ERR_INVALID_ARG;
+  if (!p->has_dev) return ELLM_ERR_NO_DEVICE;
+  p->g_wait_flag = reinterpret_cast<const uint32_t*>(p->g_win[size_t(p->g_rank)]) + layer;
+  p->g_wait_target = p->g_expect[size_t(layer)];
+  return ELLM_OK;
+}
+
 }  // extern "C"
 
 static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t* reqs, const void* q,
                           void* out, float scale, void* stream, const void* k_new, const void* v_new,
                           int64_t gather_off) {
   if (!q || !out || !std::isfinite(scale)) return ELLM_ERR_INVALID_ARG;
+  if (n > p->attn_cap) {  // a list longer than max_requests (repeated ids): grow the split-K state
+    const int rc = alloc_attn_state(p, std::max<int64_t>(n, 2 * p->attn_cap));
+    if (rc) return rc;
+  }
   const AttnShape& a = p->ash;
   const int32_t n_vr = n * a.HG;
   // descriptor cache: the same batch is attended at every layer of a decode step
@@ -1009,6 +1046,12 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
       plan.gout[i] = p->g_win[size_t(i)] + ELLM_GATHER_DATA_OFFSET + gather_off;
       plan.gflag[i] = reinterpret_cast<uint32_t*>(p->g_win[size_t(i)]) + layer;
     }
+  }
+  if (p->g_wait_flag) {  // a folded gather wait (ellm_gather_wait_next) is consumed by this launch
+    plan.wait_flag = p->g_wait_flag;
+    plan.wait_target = p->g_wait_target;
+    plan.wait_timeout_ns = p->g_timeout_ns;
+    p->g_wait_flag = nullptr;
   }
   // PDL (attention.cu): only without dynamic tickets (shared counter), with a full grid (one
   // CTA per SM, so at most this launch and the previous one overlap: a third could start only

@@ -100,6 +100,7 @@ _SIGS = {
     "ellm_gather_detach": (ctypes.c_int, [_P]),
     "ellm_attention_gather": (ctypes.c_int, [_P, _I32, _I32, _P, _V, _V, _V, _I64, ctypes.c_float, _V]),
     "ellm_gather_wait": (ctypes.c_int, [_P, _I32, _V]),
+    "ellm_gather_wait_next": (ctypes.c_int, [_P, _I32]),
     "ellm_memcpy_async": (ctypes.c_int, [_V, _V, _I64, _V]),
     "ellm_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "ellm_last_cuda_error": (ctypes.c_int, [_P]),
@@ -222,6 +223,10 @@ class Pool:
 
     def gather_wait(self, layer, stream=None) -> int:
         return ellm_gather_wait(self._h, int(layer), _sptr(stream))
+
+    def gather_wait_next(self, layer) -> int:
+        """Fold the wait for `layer`'s gather into this pool's next attention launch."""
+        return ellm_gather_wait_next(self._h, int(layer))
 
     def release(self, req, stream=None) -> int:
         return ellm_release(self._h, int(req), _sptr(stream))

@@ -3,7 +3,9 @@
 Rank i owns kv-heads [i*Hkv/N, (i+1)*Hkv/N) and their q-head groups; each rank runs its own
 pool (same T-token logical chunking with T scaled by N so chunk_bytes stays a 2 MiB multiple;
 allocation is deterministic, so every rank holds identical chunk tables). The only exchange is
-the per-layer gather of the head-sharded attention outputs, over NCCL (torch.distributed).
+the per-layer gather of the head-sharded attention outputs: fused into the attention
+kernel's merge epilogue as peer-memory stores into every rank's window (PeerGather), with
+`gather_heads` (NCCL all-gather) kept as the comparison path.
 """
 from __future__ import annotations
 

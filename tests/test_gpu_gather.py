@@ -49,13 +49,16 @@ def _oracle_check(wl_full, rows, samples, step_len, what):
         check_attention(rows[l, r][None], ref[None], f"{what} r={r} l={l}")
 
 
+@pytest.mark.parametrize("fold", [False, True], ids=["wait_kernel", "folded_wait"])
 @pytest.mark.parametrize("world,shape", [
     (2, (2, 4, 2, 64, 5, 300, 16)),        # C1-like geometry, ragged lengths via ctx 300
-    (2, (2, 32, 8, 128, 6, 2000, 16)),     # LLaMA-3-8B heads
+    (2, (3, 32, 8, 128, 6, 2000, 16)),     # LLaMA-3-8B heads
     (4, (2, 32, 8, 128, 3, 700, 16)),
-    (8, (2, 64, 8, 128, 4, 1500, 32)),     # LLaMA-70B heads, one kv-head per rank
+    (8, (3, 64, 8, 128, 4, 1500, 32)),     # LLaMA-70B heads, one kv-head per rank
 ])
-def test_gather_in_process(world, shape):
+def test_gather_in_process(world, shape, fold):
+    """fold: layer l's wait is folded into layer l+1's attention launch (gather_wait_next, with
+    launch overlap on), only the last layer's wait is a kernel — bench.py's N>1 sequence."""
     import torch
     from paper_2506_15155_b200 import ellm, shard
     from inputs import workload as W
@@ -72,6 +75,8 @@ def test_gather_in_process(world, shape):
         wins = [ellm.gather_window_create(0, nbytes)[0] for _ in range(world)]
         for i, p in enumerate(pools):
             assert p.gather_attach(world, i, Hq, wins, nbytes) == ellm.OK
+            if fold:
+                assert p.set_launch_overlap(True) == ellm.OK
         reqs, ones = list(range(B)), [1] * B
         scale = 1.0 / np.sqrt(d)
         lens = np.full(B, ctx, np.int64)
@@ -82,9 +87,12 @@ def test_gather_in_process(world, shape):
             for l in range(L):
                 for i, p in enumerate(pools):
                     q, k, v = ins[i]
+                    if fold and l > 0:
+                        assert p.gather_wait_next(l - 1) == ellm.OK
                     assert p.attention_gather(l, reqs, q[l], l * stride, scale, k[l], v[l]) == ellm.OK
-                for p in pools:
-                    assert p.gather_wait(l) == ellm.OK
+                if not fold or l == L - 1:
+                    for p in pools:
+                        assert p.gather_wait(l) == ellm.OK
         torch.cuda.synchronize()
         data = [_read_window(w, nbytes)[ellm.GATHER_DATA_OFFSET:] for w in wins]
         for i in range(1, world):
@@ -168,10 +176,15 @@ _TIMEOUT_SCRIPT = textwrap.dedent("""
 """)
 
 
-def test_gather_wait_times_out_instead_of_hanging():
+@pytest.mark.parametrize("folded", [False, True])
+def test_gather_wait_times_out_instead_of_hanging(folded):
     env = dict(os.environ, ELLM_GATHER_TIMEOUT_MS="300")
-    r = subprocess.run([sys.executable, "-c", _TIMEOUT_SCRIPT.format(root=ROOT)], env=env, capture_output=True,
-                       text=True, timeout=240)
+    script = _TIMEOUT_SCRIPT.format(root=ROOT)
+    if folded:  # the wait rides in the next attention launch's producer instead of a wait kernel
+        script = script.replace("assert pool.gather_wait(0) == 0",
+                                "assert pool.gather_wait_next(0) == 0\n"
+                                "assert pool.attention_gather(0, [0, 1], q, 0, 0.125) == 0")
+    r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=240)
     assert r.returncode == 3 and "TRAPPED" in r.stdout, (r.returncode, r.stdout[-2000:], r.stderr[-2000:])
 
 
@@ -204,9 +217,11 @@ def _ipc_worker(rank, world, port, outdir):
     for step in range(3):
         q, k, v = W.decode_inputs(wl, step, lens + step)
         assert pool.reserve(reqs, ones) == ellm.OK
-        for l in range(L):
+        for l in range(L):  # bench.py's sequence: waits folded into the next launch, then a kernel
+            if l > 0:
+                assert pool.gather_wait_next(l - 1) == ellm.OK
             assert pool.attention_gather(l, reqs, q[l], g.offset(l), scale, k[l], v[l]) == ellm.OK
-            assert pool.gather_wait(l) == ellm.OK
+        assert pool.gather_wait(L - 1) == ellm.OK
     torch.cuda.synchronize()
     np.save(os.path.join(outdir, f"win{rank}.npy"), _read_window(g.own, g.nbytes)[ellm.GATHER_DATA_OFFSET:])
     dist.barrier()  # nobody unmaps / frees while a peer may still write

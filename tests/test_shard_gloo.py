@@ -92,6 +92,8 @@ def test_gather_attach_validation_host_only():
     wins = [1 << 20, 2 << 20]
     assert pool.attention_gather(0, [0], 0, 0, 1.0) == ellm.INVALID_ARG   # not attached
     assert pool.gather_wait(0) == ellm.INVALID_ARG
+    assert pool.gather_wait_next(0) == ellm.INVALID_ARG
+    assert pool.gather_wait_next(L) == ellm.OUT_OF_RANGE
     assert pool.gather_attach(0, 0, Hq_loc, wins, nbytes) == ellm.OUT_OF_RANGE
     assert pool.gather_attach(9, 0, 9 * Hq_loc, wins * 5, nbytes) == ellm.OUT_OF_RANGE
     assert pool.gather_attach(2, 2, 2 * Hq_loc, wins, nbytes) == ellm.OUT_OF_RANGE
