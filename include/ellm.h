@@ -66,7 +66,7 @@ enum {
   ELLM_ERR_ALREADY_MAPPED = -7, /* destination chunk USED */
   ELLM_ERR_IN_USE = -8,         /* shrink needs more FREE chunks than exist */
   ELLM_ERR_CUDA = -9,           /* CUDA runtime / driver failure */
-  ELLM_ERR_NCCL = -10,          /* reserved for the fused multi-GPU path */
+  ELLM_ERR_PEER = -10,          /* a peer rank's gather window could not be opened (ellm_ipc_open) */
   ELLM_ERR_NO_DEVICE = -11,     /* call needs a device but the pool is host-metadata-only */
   ELLM_ERR_UNSUPPORTED = -12    /* shape outside what the kernels implement (see pool_create) */
 };
@@ -300,6 +300,13 @@ void* ellm_torch_alloc(size_t size, int device, void* stream);
 void ellm_torch_free(void* ptr, size_t size, int device, void* stream);
 
 /* ---- a10: head-sharded output gather fused into attention ------
+ * Boundary deviation from SURVEY §8(b): §8(b) sketches ellm_comm_init(pool, rank, world, NCCL
+ * unique id) for an NCCL communicator inside the library. The exchange here is fused into the
+ * attention kernel as peer-memory stores (no collective launch per layer), so the
+ * library needs peer windows, not a communicator: ellm_gather_window_create / ellm_ipc_open /
+ * ellm_gather_attach replace ellm_comm_init, and the 64-byte IPC handles travel over the
+ * caller's process group (torch.distributed, shard.PeerGather). NCCL stays on the caller's side
+ * only as the comparison path (bench.py --gather nccl).
  * KV-head sharding over N GPUs of one box: rank i owns kv-heads [i*Hkv/N, (i+1)*Hkv/N) and
  * q-heads [i*Hq/N, (i+1)*Hq/N) (its pool is created with the local counts). After attention
  * every rank needs all N ranks' head outputs. Instead of attention followed by an all-gather,
@@ -313,7 +320,8 @@ void ellm_torch_free(void* ptr, size_t size, int device, void* stream);
  * window_create: cudaMalloc + zero on `device` (makes it the calling thread's current device);
  *   ipc_handle_out (optional, 64 B) receives its cudaIpcMemHandle_t for the other ranks.
  * ipc_open / ipc_close: map / unmap another process's window (cudaIpcOpenMemHandle, lazy peer
- *   access). The caller owns windows and opened mappings; they must outlive the attachment.
+ *   access; a handle that cannot be opened -> ELLM_ERR_PEER). The caller owns windows and
+ *   opened mappings; they must outlive the attachment.
  * gather_attach: windows[i] = rank i's window as seen from this process (own window at
  *   windows[rank]); heads_q_total must equal world * the pool's Hq (INVALID_ARG), world in
  *   [1, 8] and rank < world (OUT_OF_RANGE), windows 256-B aligned and non-NULL. Reads this

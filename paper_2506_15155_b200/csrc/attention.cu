@@ -731,14 +731,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   __threadfence();
   for (int k = 0; k < s_n_merge; ++k) merge_request<D, 8>(p, s_merge[k], rows, NSUB, HB, 0, kConsumerWarps);
   if (p.n_peer > 0) {
-    // a10 signal: every thread's peer stores are made visible system-wide, the named barrier
-    // collects them, and thread 0 adds this CTA's merged-request count to every rank's flag with
-    // a system-scope release. A rank's flag reaches world * n_vr once all ranks' rows are in.
+    // a10 signal: the named barrier orders every consumer thread's row stores before thread 0,
+    // whose system-scope release (cumulative over what the barrier made it observe) then adds
+    // this CTA's merged-request count to every rank's flag. A rank's flag reaches world * n_vr
+    // once all ranks' rows are in. (No per-thread membar.sys: the release covers them.)
     const int merged = s_n_merge + s_n_now;
-    __threadfence_system();
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
     if (threadIdx.x == 0 && merged > 0) {
-      __threadfence_system();
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
       for (int i = 0; i < p.n_peer; ++i)
         asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p.gflag[i]), "r"(merged) : "memory");
     }

@@ -5,6 +5,7 @@
 // All three are HBM- (or host-link-) bound byte copies: 16-byte vector accesses, several
 // independent loads in flight per thread before the stores, grids sized to the SM count.
 #include <cstdio>
+#include <cstdlib>
 #include "internal.h"
 
 namespace ellm {
@@ -117,6 +118,101 @@ __global__ void __launch_bounds__(256) chunk_copy_kernel(uint8_t* __restrict__ d
   }
 }
 
+// D2D chunk copy (migrate, a8) through the TMA engine: one CTA per SM, one issuing thread.
+// Units of kBulkUnit bytes go global -> shared (cp.async.bulk, mbarrier completion) into a ring of
+// kBulkStages slots and shared -> global (cp.async.bulk store, bulk-group completion); a slot is
+// reloaded as soon as the store issued kBulkLag iterations earlier has finished reading it, so
+// ~kBulkStages units (~176 KiB) per SM are in flight with no register staging. Work is claimed
+// kBulkGrab units per atomic, the next grab fetched before the current one is streamed.
+constexpr int kBulkUnit = 16384;
+constexpr int kBulkStages = 11;
+constexpr int kBulkLag = 2;
+constexpr int kBulkGrab = 4;
+constexpr int kBulkSmem = kBulkStages * kBulkUnit + 1024;
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__global__ void __launch_bounds__(32, 1) chunk_copy_bulk_kernel(uint8_t* __restrict__ dst_base,
+                                                                const int32_t* __restrict__ dst_idx,
+                                                                const uint8_t* __restrict__ src_base,
+                                                                const int32_t* __restrict__ src_idx,
+                                                                int32_t n, int64_t chunk_bytes,
+                                                                uint32_t* __restrict__ work, int32_t rot,
+                                                                int64_t slab) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ alignas(8) uint64_t full[kBulkStages];
+  if (threadIdx.x != 0) return;
+  uint8_t* buf = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  const uint32_t sbuf = smem_addr(buf);
+  for (int s = 0; s < kBulkStages; ++s)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[s])) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const int64_t upc = chunk_bytes / kBulkUnit;
+  const int64_t total = int64_t(n) * upc;
+  int64_t cur = 0, end = 0;                          // current grab [cur, end)
+  uint32_t next_g = atomicAdd(work, 1u);             // the following grab, claimed ahead
+  auto next_unit = [&]() -> int64_t {
+    if (cur >= end) {
+      cur = int64_t(next_g) * kBulkGrab;
+      if (cur >= total) return -1;
+      end = cur + kBulkGrab < total ? cur + kBulkGrab : total;
+      next_g = atomicAdd(work, 1u);
+    }
+    return cur++;
+  };
+  auto addr = [&](int64_t w, bool dst) -> uint8_t* {
+    const int64_t i = w / upc, off = (w % upc) * int64_t(kBulkUnit);  // canonical offset
+    const int64_t c = __ldg((dst ? dst_idx : src_idx) + i);
+    int64_t o = off;
+    if (rot) {
+      const int32_t l = int32_t(off / slab);
+      o = int64_t(slab_slot(c, l, rot)) * slab + (off - int64_t(l) * slab);
+    }
+    return (dst ? dst_base : const_cast<uint8_t*>(src_base)) + c * chunk_bytes + o;
+  };
+  uint8_t* dptr[kBulkStages];
+  int64_t nload = 0, nstore = 0;
+  bool more = true;
+  auto issue_load = [&]() {
+    const int64_t w = next_unit();
+    if (w < 0) {
+      more = false;
+      return;
+    }
+    const int st = int(nload % kBulkStages);
+    const uint32_t bar = smem_addr(&full[st]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kBulkUnit) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(sbuf + st * kBulkUnit), "l"(addr(w, false)), "r"(kBulkUnit), "r"(bar) : "memory");
+#pragma unroll
+    for (int k = 0; k < kBulkStages; ++k)
+      if (k == st) dptr[k] = addr(w, true);  // select: keeps dptr[] in registers
+    ++nload;
+  };
+  while (more && nload < kBulkStages) issue_load();
+  while (nstore < nload) {
+    const int st = int(nstore % kBulkStages);
+    const uint32_t par = uint32_t(nstore / kBulkStages) & 1u;
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W_%=;\n}" ::"r"(smem_addr(&full[st])), "r"(par) : "memory");
+    uint8_t* d = dptr[0];
+#pragma unroll
+    for (int k = 1; k < kBulkStages; ++k)
+      if (k == st) d = dptr[k];
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 ::"l"(d), "r"(sbuf + st * kBulkUnit), "r"(kBulkUnit) : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    ++nstore;
+    // stores up to nstore-1-kBulkLag have read their slot: refill slots up to that one
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kBulkLag) : "memory");
+    while (more && nload < nstore - kBulkLag + kBulkStages) issue_load();
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 }  // namespace
 
 cudaError_t launch_table_scatter(int32_t* d_table, const TableUpdate* d_updates, int32_t n,
@@ -151,6 +247,24 @@ cudaError_t launch_chunk_copy(uint8_t* dst_base, const int32_t* dst_idx, const u
   if (seg_bytes % kCopyUnit != 0 || seg_off % 16 != 0 || seg_off + seg_bytes > chunk_bytes)
     return cudaErrorInvalidValue;
   if (rot && (slab % kCopyUnit != 0 || seg_off % kCopyUnit != 0)) return cudaErrorInvalidValue;
+  const char* bulk_e = std::getenv("ELLM_D2D_BULK");  // 0: the warp copy kernel (comparison)
+  const int bulk_env = bulk_e ? std::atoi(bulk_e) : -1;
+  if (src_dev && dst_dev && seg_off == 0 && seg_bytes == chunk_bytes && chunk_bytes % kBulkUnit == 0 &&
+      (!rot || slab % kBulkUnit == 0) && bulk_env != 0) {  // whole-chunk D2D: TMA bulk copy
+    static bool configured = false;
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(chunk_copy_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kBulkSmem);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+    const int64_t bunits = int64_t(n) * (chunk_bytes / kBulkUnit);
+    const int64_t bneed = (bunits + kBulkGrab - 1) / kBulkGrab;
+    const int bgrid = int(std::max<int64_t>(1, std::min<int64_t>(grid / 2, bneed)));  // grid = 2 x #SM
+    chunk_copy_bulk_kernel<<<bgrid, 32, kBulkSmem, s>>>(dst_base, dst_idx, src_base, src_idx, n, chunk_bytes,
+                                                       work, rot, slab);
+    return cudaGetLastError();
+  }
   int64_t units = int64_t(n) * (seg_bytes / kCopyUnit);
   int64_t need = (units + 8 * kCopyGrab - 1) / (8 * kCopyGrab);  // one grab per warp at least
   grid = int(std::max<int64_t>(1, std::min<int64_t>(grid, need)));

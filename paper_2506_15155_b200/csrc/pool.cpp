@@ -388,7 +388,7 @@ const char* ellm_status_string(int s) {
     case ELLM_ERR_ALREADY_MAPPED: return "destination already in use";
     case ELLM_ERR_IN_USE: return "chunks in use";
     case ELLM_ERR_CUDA: return "CUDA error";
-    case ELLM_ERR_NCCL: return "NCCL error";
+    case ELLM_ERR_PEER: return "peer gather window could not be opened";
     case ELLM_ERR_NO_DEVICE: return "pool has no device";
     case ELLM_ERR_UNSUPPORTED: return "unsupported shape";
     default: return "unknown status";
@@ -801,7 +801,9 @@ int ellm_ipc_open(const void* ipc_handle, void** window_out) {
   cudaIpcMemHandle_t h;
   std::memcpy(&h, ipc_handle, sizeof(h));
   cudaError_t e = cudaIpcOpenMemHandle(window_out, h, cudaIpcMemLazyEnablePeerAccess);
-  return e == cudaSuccess ? ELLM_OK : cuda_fail(nullptr, e);
+  if (e == cudaSuccess) return ELLM_OK;
+  cudaGetLastError();  // not sticky: clear it
+  return ELLM_ERR_PEER;
 }
 
 int ellm_ipc_close(void* window) {

@@ -18,11 +18,11 @@ LIB_PATH = os.path.join(_HERE, "libellm.so")
 OK = 0
 ERR = {
     -1: "INVALID_ARG", -2: "OUT_OF_RANGE", -3: "NO_CHUNKS", -4: "HOST_FULL", -5: "NOT_RESIDENT",
-    -6: "NOT_MAPPED", -7: "ALREADY_MAPPED", -8: "IN_USE", -9: "CUDA", -10: "NCCL", -11: "NO_DEVICE",
+    -6: "NOT_MAPPED", -7: "ALREADY_MAPPED", -8: "IN_USE", -9: "CUDA", -10: "PEER", -11: "NO_DEVICE",
     -12: "UNSUPPORTED",
 }
 (INVALID_ARG, OUT_OF_RANGE, NO_CHUNKS, HOST_FULL, NOT_RESIDENT, NOT_MAPPED, ALREADY_MAPPED, IN_USE,
- CUDA, NCCL, NO_DEVICE, UNSUPPORTED) = range(-1, -13, -1)
+ CUDA, PEER, NO_DEVICE, UNSUPPORTED) = range(-1, -13, -1)
 DEVICE_NONE = -1
 
 if not os.path.exists(LIB_PATH):

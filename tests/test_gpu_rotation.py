@@ -14,9 +14,11 @@ from tests.twin import Twin
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("bulk", ["1", "0"], ids=["tma_migrate", "warp_migrate"])
 @pytest.mark.parametrize("rotate", ["1", "0"])
-def test_rotated_slabs_match_oracle(rotate, monkeypatch):
+def test_rotated_slabs_match_oracle(rotate, bulk, monkeypatch):
     monkeypatch.setenv("ELLM_ROTATE", rotate)
+    monkeypatch.setenv("ELLM_D2D_BULK", bulk)  # migrate through the TMA bulk kernel or the warp kernel
     rng = np.random.default_rng(3)
     L, Hq, Hkv, d, T = 3, 8, 2, 128, 16          # chunk 48 KiB, slab 16 KiB
     R, MC, C, H = 6, 48, 224, 160                 # 7 rotation groups of 32 chunks

@@ -93,6 +93,11 @@ def test_gather_attach_validation_host_only():
     assert pool.attention_gather(0, [0], 0, 0, 1.0) == ellm.INVALID_ARG   # not attached
     assert pool.gather_wait(0) == ellm.INVALID_ARG
     assert pool.gather_wait_next(0) == ellm.INVALID_ARG
+    try:  # a handle that cannot be opened (here: no device at all) is a peer failure
+        ellm.ipc_open(bytes(ellm.IPC_HANDLE_BYTES))
+        raise AssertionError("ipc_open of a null handle succeeded")
+    except ellm.EllmError as e:
+        assert e.rc == ellm.PEER, e
     assert pool.gather_wait_next(L) == ellm.OUT_OF_RANGE
     assert pool.gather_attach(0, 0, Hq_loc, wins, nbytes) == ellm.OUT_OF_RANGE
     assert pool.gather_attach(9, 0, 9 * Hq_loc, wins * 5, nbytes) == ellm.OUT_OF_RANGE
