@@ -1093,7 +1093,10 @@ def measure_swap(pool, wl, stream):
     sp = stream.cuda_stream
 
     def timed(fn):
+        # device time of the call: a sleep kernel holds the stream while the host enqueues the
+        # call (index upload + kernel / copies), so the events bracket only its device work
         torch.cuda.synchronize()
+        torch.cuda._sleep(20_000_000)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         r = fn()

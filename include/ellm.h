@@ -311,8 +311,9 @@ void ellm_torch_free(void* ptr, size_t size, int device, void* stream);
  * q-heads [i*Hq/N, (i+1)*Hq/N) (its pool is created with the local counts). After attention
  * every rank needs all N ranks' head outputs. Instead of attention followed by an all-gather,
  * the attention kernel's split-K merge stores each finished output row directly into EVERY
- * rank's gather window over peer memory (NVLink P2P stores), and each CTA then adds the number
- * of requests it merged to every rank's flag word for that layer (release, system scope).
+ * rank's gather window over peer memory (NVLink P2P stores); the CTAs count their completion at
+ * GPU scope and the last one adds the call's request count to every rank's flag word for that
+ * layer (one system-scope release per call).
  * A gather window is one device allocation per rank, identical size on all ranks:
  *   [0, ELLM_GATHER_DATA_OFFSET)     uint32 flag words, one per layer (monotone counters)
  *   [ELLM_GATHER_DATA_OFFSET, bytes) rows: a call with out_offset writes [n, Hq_total, d] bf16

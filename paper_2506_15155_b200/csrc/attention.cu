@@ -23,6 +23,7 @@
 //    request (per-request arrival counter) merges its partials with the log-sum-exp rule and
 //    writes the bf16 output, so one launch does rows a4 and a5.
 #include <cstdio>
+#include <cstdlib>
 
 #include <cuda_bf16.h>
 
@@ -154,8 +155,8 @@ struct Params {
   float scale_log2;
   // a10 fused head gather (n_peer > 0; ellm_attention_gather): each merged output row is stored
   // into EVERY rank's gather window over peer memory (NVLink P2P), at global q-head
-  // q_off + local head of a [n, Hq_out, D] layout, instead of into `out`; each CTA then adds the
-  // number of requests it merged to every rank's flag word (release, system scope).
+  // q_off + local head of a [n, Hq_out, D] layout, instead of into `out`; the launch's last CTA to
+  // finish then adds the launch's n_vr to every rank's flag word (release, system scope).
   __nv_bfloat16* gout[kMaxPeers];
   uint32_t* gflag[kMaxPeers];
   int32_t n_peer, Hq_out, q_off;
@@ -165,6 +166,9 @@ struct Params {
   const uint32_t* wait_flag;
   uint32_t wait_target;
   unsigned long long wait_timeout_ns;
+  int32_t gscope_gpu;  // 1: gather release at gpu scope (measurement knob, single-device windows only)
+  uint32_t* gdone;     // gather launches: CTAs finished (monotone counter) and this launch's final value
+  uint32_t gdone_target;
 };
 constexpr int kFirst = 1, kLast = 2, kDone = 4;  // stage metadata flags
 
@@ -731,16 +735,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   __threadfence();
   for (int k = 0; k < s_n_merge; ++k) merge_request<D, 8>(p, s_merge[k], rows, NSUB, HB, 0, kConsumerWarps);
   if (p.n_peer > 0) {
-    // a10 signal: the named barrier orders every consumer thread's row stores before thread 0,
-    // whose system-scope release (cumulative over what the barrier made it observe) then adds
-    // this CTA's merged-request count to every rank's flag. A rank's flag reaches world * n_vr
-    // once all ranks' rows are in. (No per-thread membar.sys: the release covers them.)
-    const int merged = s_n_merge + s_n_now;
+    // a10 signal. Every CTA orders its row stores before a gpu-scope count (the named barrier
+    // gathers the consumer threads' stores at thread 0, whose acq_rel fence + relaxed add is a
+    // release); the CTA whose add completes the launch's count has then observed every CTA's
+    // rows, and one system-scope fence (cumulative) + a relaxed add of all n_vr merged requests
+    // to every rank's flag publishes them. One membar.sys per launch instead of one per CTA
+    // (measured: a membar.sys in every CTA cost ~6 us of a 50 us 8-way launch).
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
-    if (threadIdx.x == 0 && merged > 0) {
-      asm volatile("fence.acq_rel.sys;" ::: "memory");
-      for (int i = 0; i < p.n_peer; ++i)
-        asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p.gflag[i]), "r"(merged) : "memory");
+    if (threadIdx.x == 0) {
+      uint32_t old;
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p.gdone) : "memory");
+      if (old == p.gdone_target - 1u) {
+        const uint32_t all = uint32_t(p.n_vr);
+        if (p.gscope_gpu) {  // measurement knob (ELLM_GATHER_SCOPE=gpu): every window on this device
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          for (int i = 0; i < p.n_peer; ++i)
+            asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p.gflag[i]), "r"(all) : "memory");
+        } else {
+          asm volatile("fence.acq_rel.sys;" ::: "memory");
+          for (int i = 0; i < p.n_peer; ++i)
+            asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p.gflag[i]), "r"(all) : "memory");
+        }
+      }
     }
   }
 }
@@ -855,9 +872,15 @@ cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh,
     prm.gout[i] = static_cast<__nv_bfloat16*>(plan.gout[i]);
     prm.gflag[i] = plan.gflag[i];
   }
+  prm.gdone = plan.gdone;
+  prm.gdone_target = plan.gdone_target;
   prm.wait_flag = plan.wait_flag;
   prm.wait_target = plan.wait_target;
   prm.wait_timeout_ns = plan.wait_timeout_ns;
+  {
+    const char* g = std::getenv("ELLM_GATHER_SCOPE");
+    prm.gscope_gpu = (g && g[0] == 'g') ? 1 : 0;
+  }
   cudaError_t e;
   if (sh.D == 128) {
     switch (sh.HB) {

@@ -165,6 +165,8 @@ struct AttnPlan {
   void* gout[kMaxPeers] = {};
   uint32_t* gflag[kMaxPeers] = {};
   int32_t n_peer = 0, Hq_out = 0, q_off = 0;
+  uint32_t* gdone = nullptr;   // CTAs of gather launches that finished (device counter)
+  uint32_t gdone_target = 0;   // value the counter reaches when this launch's last CTA arrives
   // a10 folded gather wait (ellm_gather_wait_next): before staging Q or writing anything, the
   // producer spins (acquire, system scope) until *wait_flag reaches wait_target; nullptr = none
   const uint32_t* wait_flag = nullptr;
@@ -274,6 +276,7 @@ struct ellm_pool {
   ellm::AttnPlan cache_plan;
   unsigned long long* d_ticket = nullptr;  // dynamic-unit ticket counter (device)
   uint64_t ticket_base = 0;                // tickets consumed by earlier launches
+  uint32_t gdone_base = 0;                 // gather-launch CTAs counted by earlier launches
   int64_t dyn_div = 0;                     // dynamic tail = tiles/dyn_div per request (0: static only)
   int64_t dyn_unit = 8;                    // minimum tiles per dynamic unit
 

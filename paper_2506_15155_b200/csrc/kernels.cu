@@ -247,10 +247,14 @@ cudaError_t launch_chunk_copy(uint8_t* dst_base, const int32_t* dst_idx, const u
   if (seg_bytes % kCopyUnit != 0 || seg_off % 16 != 0 || seg_off + seg_bytes > chunk_bytes)
     return cudaErrorInvalidValue;
   if (rot && (slab % kCopyUnit != 0 || seg_off % kCopyUnit != 0)) return cudaErrorInvalidValue;
-  const char* bulk_e = std::getenv("ELLM_D2D_BULK");  // 0: the warp copy kernel (comparison)
-  const int bulk_env = bulk_e ? std::atoi(bulk_e) : -1;
+  // Whole-chunk D2D: the TMA bulk kernel by default when chunk_bytes is a power of two (C2's
+  // 2 MiB chunks: 6534 vs 6298 GB/s device time); with 10 MiB rotated chunks the warp kernel is
+  // faster (6347 vs 4615 GB/s, tools/migrate_probe.py). ELLM_D2D_BULK=1 / 0 forces either.
+  const char* bulk_e = std::getenv("ELLM_D2D_BULK");
+  const bool pow2 = (chunk_bytes & (chunk_bytes - 1)) == 0;
+  const bool want_bulk = bulk_e ? std::atoi(bulk_e) != 0 : pow2;
   if (src_dev && dst_dev && seg_off == 0 && seg_bytes == chunk_bytes && chunk_bytes % kBulkUnit == 0 &&
-      (!rot || slab % kBulkUnit == 0) && bulk_env != 0) {  // whole-chunk D2D: TMA bulk copy
+      (!rot || slab % kBulkUnit == 0) && want_bulk) {
     static bool configured = false;
     if (!configured) {
       cudaError_t e = cudaFuncSetAttribute(chunk_copy_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

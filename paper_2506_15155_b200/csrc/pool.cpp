@@ -559,8 +559,9 @@ int ellm_pool_create(const ellm_pool_config* cfg, ellm_pool** out) {
   if (const char* v = std::getenv("ELLM_ROTATE")) want_rot = std::atoi(v) != 0;
   a.rot = (can_rot && want_rot) ? c.n_layers : 0;
   if ((rc = alloc_attn_state(p, c.max_requests))) return fail(rc);
-  if ((e = cudaMalloc(reinterpret_cast<void**>(&p->d_ticket), 8)) != cudaSuccess ||
-      (e = cudaMemset(p->d_ticket, 0, 8)) != cudaSuccess)
+  // d_ticket[0]: dynamic-unit tickets; d_ticket[1] (low word): CTAs finished in gather launches
+  if ((e = cudaMalloc(reinterpret_cast<void**>(&p->d_ticket), 16)) != cudaSuccess ||
+      (e = cudaMemset(p->d_ticket, 0, 16)) != cudaSuccess)
     return fail(cuda_fail(p, e));
   if ((rc = p->ring.init(size_t(1) << 20, 16))) return fail(rc);
   if ((e = encode_kv_tensor_map(&p->tmap, ellm_vtensor_base(p->vt), c.max_chunks, a)) != cudaSuccess)
@@ -1048,6 +1049,9 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
       plan.gout[i] = p->g_win[size_t(i)] + ELLM_GATHER_DATA_OFFSET + gather_off;
       plan.gflag[i] = reinterpret_cast<uint32_t*>(p->g_win[size_t(i)]) + layer;
     }
+    // the CTA that finishes last (gpu-scope count, monotone across launches) signals every rank
+    plan.gdone = reinterpret_cast<uint32_t*>(p->d_ticket + 1);
+    plan.gdone_target = p->gdone_base + uint32_t(plan.G);
   }
   if (p->g_wait_flag) {  // a folded gather wait (ellm_gather_wait_next) is consumed by this launch
     plan.wait_flag = p->g_wait_flag;
@@ -1075,7 +1079,10 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
   // tickets consumed: every unit once, plus the two outstanding tickets each CTA ends with
   if (plan.n_dyn > 0) p->ticket_base += uint64_t(plan.n_dyn) + 2 * uint64_t(plan.G);
   // every rank merges its n_vr requests once and adds them to every rank's flag word
-  if (gather_off >= 0) p->g_expect[size_t(layer)] += uint32_t(p->g_world) * uint32_t(n_vr);
+  if (gather_off >= 0) {
+    p->g_expect[size_t(layer)] += uint32_t(p->g_world) * uint32_t(n_vr);
+    p->gdone_base += uint32_t(plan.G);
+  }
   return upload ? p->ring.commit(S(stream)) : p->ring.commit_lazy(S(stream));
 }
 
@@ -1610,7 +1617,7 @@ int ellm_prefill_attention(ellm_pool* p, int32_t layer, int32_t n, const int32_t
   if (n == 0) return ELLM_OK;
   cudaStream_t st = S(stream);
   if (int rc = flush_table(p, st)) return rc;
-  const int bp = 128 / p->group;  // query positions per block
+  const int bp = 256 / p->group;  // query positions per work item: two Q tiles of 128 rows (prefill.cu)
   struct Item { int32_t v[8]; };
   std::vector<Item> items;
   int64_t row0 = 0;

@@ -28,26 +28,26 @@
 namespace ellm {
 namespace {
 
-constexpr int kM = 128;         // MMA rows per CTA
+constexpr int kM = 128;         // MMA rows per Q tile (TMEM lanes)
 constexpr int kN = 128;         // keys per tile
-constexpr int kKStages = 3;     // K ring depth: K(t+2) is requested while S(t) / softmax(t) run
+constexpr int kQTiles = 2;      // Q tiles per CTA (ping-pong: one tile's softmax hides the other's MMAs)
+constexpr int kKStages = 2;     // K ring depth
 constexpr int kVStages = 2;     // V ring depth
-constexpr int kThreads = 192;   // warp 0 TMA, warp 1 MMA, warps 2..5 softmax
+constexpr int kSoftmaxWarps = 4 * kQTiles;
+constexpr int kThreads = 64 + 32 * kSoftmaxWarps;  // warp 0 TMA, warp 1 MMA, 4 softmax warps per Q tile
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleHeadroom = 8.f;  // log2 units: P <= 2^8 before O is rescaled
 
 template <int D>
 struct Layout {
-  static constexpr int TILE = kN * D * 2;  // one K or V tile: [D/64][128 tokens][64] bf16
-  static constexpr int Q = kM * D * 2;     // [D/64][128 rows][64]
-  static constexpr int P = kM * kN * 2;    // one P buffer: [2 token halves][128 rows][64]
-  static constexpr int off_q = 0;
-  static constexpr int off_k = Q;          // K stage s at off_k + s*TILE
-  static constexpr int off_v = off_k + kKStages * TILE;  // V stage s at off_v + s*TILE
-  static constexpr int off_p = off_v + kVStages * TILE;
-  static constexpr int off_bar = off_p + P;  // one P buffer (its reuse waits for P.V of the tile before)
-  // >= 116 KB so one CTA owns an SM (its 512 TMEM columns are the whole TMEM)
-  static constexpr int bytes = (off_bar + 256 + 1024) > 118784 ? (off_bar + 256 + 1024) : 118784;
+  static constexpr int TILE = kN * D * 2;   // one K or V tile: [D/64][128 tokens][64] bf16
+  static constexpr int QT = kM * D * 2;     // one Q tile: [D/64][128 rows][64]
+  static constexpr int off_q = 0;           // Q tile x at off_q + x*QT
+  static constexpr int off_k = kQTiles * QT;                // K stage s at off_k + s*TILE
+  static constexpr int off_v = off_k + kKStages * TILE;     // V stage s at off_v + s*TILE
+  static constexpr int off_bar = off_v + kVStages * TILE;
+  static constexpr int bytes = off_bar + 256 + 1024;
+  static_assert(bytes <= 232448, "shared memory per CTA");
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -150,8 +150,38 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
       : "memory");
 }
 #undef ELLM_W32
+#define ELLM_R16(i) "=r"(r[i])
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15}, [%16];"
+      : ELLM_R16(0), ELLM_R16(1), ELLM_R16(2), ELLM_R16(3), ELLM_R16(4), ELLM_R16(5), ELLM_R16(6), ELLM_R16(7),
+        ELLM_R16(8), ELLM_R16(9), ELLM_R16(10), ELLM_R16(11), ELLM_R16(12), ELLM_R16(13), ELLM_R16(14),
+        ELLM_R16(15)
+      : "r"(taddr));
+}
+#undef ELLM_R16
+#define ELLM_W16(i) "r"(r[i])
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16};" ::"r"(taddr),
+      ELLM_W16(0), ELLM_W16(1), ELLM_W16(2), ELLM_W16(3), ELLM_W16(4), ELLM_W16(5), ELLM_W16(6), ELLM_W16(7),
+      ELLM_W16(8), ELLM_W16(9), ELLM_W16(10), ELLM_W16(11), ELLM_W16(12), ELLM_W16(13), ELLM_W16(14), ELLM_W16(15)
+      : "memory");
+}
+#undef ELLM_W16
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// A operand from tensor memory (P: M=128 lanes x K keys, two bf16 per 32-bit column)
+__device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
 
 struct PParams {
   const int4* work;        // [n_work][2]: {req, len, q_row0, p0}, {n_valid, kvh, n_tiles, 0}
@@ -163,6 +193,12 @@ struct PParams {
   float scale_log2;
 };
 
+// One CTA per work item = (request, kv-head, block of 2 x 128/group query positions): Q tile x
+// (x = 0, 1) holds the block's x-th 128/group positions x group heads as its M = 128 rows.
+// TMEM (512 columns): S_x at [128x, 128x + 128) — overwritten in place by P_x as bf16 pairs in its
+// first 64 columns — and O_x at [256 + 128x, 256 + 128x + D). Both tiles share every K/V tile.
+// The MMA thread issues, per key tile t:  PV_0(t), S_0(t+1), PV_1(t), S_1(t+1), so while softmax
+// warpgroup x works on S_x(t+1) the tensor pipe runs the other tile's P.V and S.
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     prefill_kernel(const __grid_constant__ PrefillMaps maps, const PParams p) {
@@ -172,20 +208,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sb = smem_u32(smem);
   const uint32_t bar0 = sb + LY::off_bar;
-  // barriers: q_full, k_full[3], k_empty[3], v_full[2], v_empty[2], s_full[2], p_full[2],
-  // pv_done[2]; then the TMEM address. K and V slots are released separately (K(t) right after
-  // S(t)); the K ring is 3 deep so K(t+2) is in flight during softmax(t) (ncu: softmax warps
-  // waited on S, i.e. on K from L2, with a 2-deep ring). The single P buffer is rewritten once
-  // P.V of the previous tile has read it; the exponentials are computed before that wait.
-  const uint32_t q_full = bar0, k_full = bar0 + 8, k_empty = bar0 + 32, v_full = bar0 + 56,
-                 v_empty = bar0 + 72, s_full = bar0 + 88, p_full = bar0 + 104, pv_done = bar0 + 120;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + LY::off_bar + 192);
+  // barriers (8 B each): q_full, k_full[KS], k_empty[KS], v_full[VS], v_empty[VS],
+  // s_full[2], p_full[2], o_full[2]; then the TMEM address
+  const uint32_t q_full = bar0, k_full = bar0 + 8, k_empty = k_full + 8 * kKStages,
+                 v_full = k_empty + 8 * kKStages, v_empty = v_full + 8 * kVStages,
+                 s_full = v_empty + 8 * kVStages, p_full = s_full + 16, o_full = p_full + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + LY::off_bar + 224);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int4 w0 = p.work[2 * blockIdx.x], w1 = p.work[2 * blockIdx.x + 1];
   const int req = w0.x, q_row0 = w0.z, p0 = w0.w;
   const int n_valid = w1.x, kvh = w1.y, n_tiles = w1.z;
   const int last_key = p0 + n_valid - 1;  // the block's largest query position (< len)
+  const int bp = kM / p.group;             // positions per Q tile
+  const int nq = n_valid > bp ? 2 : 1;     // Q tiles with any valid row
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
@@ -193,17 +229,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(k_full + 8 * s, 1);
       mbar_init(k_empty + 8 * s, 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kVStages; ++s) {
       mbar_init(v_full + 8 * s, 1);
       mbar_init(v_empty + 8 * s, 1);
-      mbar_init(s_full + 8 * s, 1);
-      mbar_init(p_full + 8 * s, 4);
-      mbar_init(pv_done + 8 * s, 1);
+    }
+    for (int x = 0; x < kQTiles; ++x) {
+      mbar_init(s_full + 8 * x, 1);
+      mbar_init(p_full + 8 * x, 4);
+      mbar_init(o_full + 8 * x, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
-  if (warp == 1) {  // TMEM: S0 [0,128), S1 [128,256), O [256, 256 + D)
+  if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(kTmemCols)
                  : "memory");
@@ -216,15 +254,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ================================ TMA producer ================================
-    // The whole warp walks the chunk table (lane k: piece k of a tile, loaded one tile ahead so
-    // the load latency hides behind the barrier waits); lane 0 issues the TMAs.
+    // The whole warp walks the chunk table (lane k: piece k of a tile, loaded ahead so the load
+    // latency hides behind the barrier waits); lane 0 issues the TMAs.
     uint64_t policy;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy));
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.kv)) : "memory");
-      mbar_expect_tx(q_full, uint32_t(LY::Q));
-      for (int h = 0; h < HALVES; ++h)  // box {64, group heads, 1 half, 128/group rows}
-        tma_4d(sb + LY::off_q + h * kM * 128, &maps.q, 0, kvh * p.group, h, q_row0, q_full);
+      mbar_expect_tx(q_full, uint32_t(nq * LY::QT));
+      for (int x = 0; x < nq; ++x)
+        for (int h = 0; h < HALVES; ++h)  // box {64, group heads, 1 half, 128/group rows}
+          tma_4d(sb + LY::off_q + x * LY::QT + h * kM * 128, &maps.q, 0, kvh * p.group, h, q_row0 + x * bp, q_full);
     }
     const int tp = p.T < kN ? p.T : kN;  // tokens per chunk piece
     const int32_t* trow = p.table + int64_t(req) * p.table_stride;
@@ -232,16 +271,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto load_ent = [&](int t) {
       return (t < n_tiles && lane < pieces(t)) ? __ldg(trow + (t * kN + lane * tp) / p.T) : -1;
     };
-    // order: K(0), K(1), K(2), V(0), K(3), V(1), ... — K runs two tiles ahead of V
     auto issue = [&](int t, int kv, int e) {
-      const int s = kv ? (t & 1) : (t % kKStages);
-      const int round = kv ? (t >> 1) : (t / kKStages);
+      const int ns = kv ? kVStages : kKStages;
+      const int s = t % ns, round = t / ns;
       const uint32_t full = (kv ? v_full : k_full) + 8 * s, empty = (kv ? v_empty : k_empty) + 8 * s;
       const int npc = pieces(t);
       const uint32_t dst = sb + (kv ? LY::off_v : LY::off_k) + s * LY::TILE;
-      // runs of consecutive chunk ids go as one box of 1/2/4/8 chunks (TMA issue cost is per box)
-      const int prev = __shfl_up_sync(0xffffffffu, e, 1);
+      // runs of consecutive chunk ids go as one box of 1/2/4/8 chunks (TMA issue cost is per box);
       // with rotated slabs a run also breaks at a rotation-group boundary (the slot changes there)
+      const int prev = __shfl_up_sync(0xffffffffu, e, 1);
       unsigned starts = __ballot_sync(
           0xffffffffu, lane < npc && (lane == 0 || e != prev + 1 || p.T >= kN || !p.runs ||
                                       (p.rot && e % kRotGroup == 0)));
@@ -261,8 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_5d(dst + h * kN * 128 + k * tp * 128, &maps.kv, 0, p.T >= kN ? (t * kN) % p.T : 0, h, kvh,
                      (c * p.L + sl) * 2 + kv, full, policy);
           } else {
-            // run map dim 3: (kv, head) blocks over the whole pool; dim 4 steps one chunk (+ one
-            // slab when rotated: consecutive chunks' slots advance by one) — see encode below
+            // run map dim 3: (kv, head) blocks over the whole pool; dim 4 steps one chunk
             const int c3 = (sl * 2 + kv) * p.Hkv + kvh;  // the run's slot: constant inside it
             for (int done = 0; done < kend - k;) {
               const int lg = min(3, 31 - __clz(kend - k - done));
@@ -276,16 +313,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
     };
-    int e_cur = load_ent(0), e_n1 = load_ent(1), e_n2 = load_ent(2);
+    // order: K(0), K(1), V(0), K(2), V(1), ... — K one tile ahead of V
+    int e_cur = load_ent(0), e_n1 = load_ent(1);
     issue(0, 0, e_cur);
-    if (n_tiles > 1) issue(1, 0, e_n1);
     for (int t = 0; t < n_tiles; ++t) {
-      const int e_after = load_ent(t + 3);  // in flight while this iteration waits
-      if (t + 2 < n_tiles) issue(t + 2, 0, e_n2);
+      const int e_after = load_ent(t + 2);  // in flight while this iteration waits
+      if (t + 1 < n_tiles) issue(t + 1, 0, e_n1);
       issue(t, 1, e_cur);
       e_cur = e_n1;
-      e_n1 = e_n2;
-      e_n2 = e_after;
+      e_n1 = e_after;
     }
   } else if (warp == 1) {
     // ================================ MMA issuer ================================
@@ -293,143 +329,152 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t id_s = idesc_bf16(kM, kN, false);
       constexpr uint32_t id_pv = idesc_bf16(kM, D, true);
       mbar_wait(q_full, 0);
-      auto issue_s = [&](int t) {
-        const int s = t & 1, ks = t % kKStages;
-        mbar_wait(k_full + 8 * ks, (t / kKStages) & 1);
-        tc_fence_after();
-        const uint32_t kb = sb + LY::off_k + ks * LY::TILE;
+      auto issue_s = [&](int x, int t) {  // S_x(t) = Q_x K(t)^T into TMEM columns [128x, 128x + 128)
+        const uint32_t kb = sb + LY::off_k + (t % kKStages) * LY::TILE;
+        const uint32_t qb = sb + LY::off_q + x * LY::QT;
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * (kM * 128) + (k & 3) * 32;
-          umma(tmem + s * 128, desc_sw128(sb + LY::off_q + off, 16), desc_sw128(kb + off, 16), id_s, k > 0);
+          umma(tmem + x * 128, desc_sw128(qb + off, 16), desc_sw128(kb + off, 16), id_s, k > 0);
         }
-        umma_commit(s_full + 8 * s);
-        umma_commit(k_empty + 8 * ks);
+        umma_commit(s_full + 8 * x);
       };
-      issue_s(0);
-      for (int t = 0; t < n_tiles; ++t) {
-        if (t + 1 < n_tiles) issue_s(t + 1);
-        mbar_wait(p_full + 8 * (t & 1), (t >> 1) & 1);
-        mbar_wait(v_full + 8 * (t & 1), (t >> 1) & 1);
+      auto issue_pv = [&](int x, int t) {  // O_x += P_x(t) V(t), P_x from TMEM (S_x's columns)
+        mbar_wait(p_full + 8 * x, t & 1);
         tc_fence_after();
-        const uint32_t vb = sb + LY::off_v + (t & 1) * LY::TILE;
+        const uint32_t vb = sb + LY::off_v + (t % kVStages) * LY::TILE;
 #pragma unroll
         for (int k = 0; k < kN / 16; ++k)
-          umma(tmem + 256, desc_sw128(sb + LY::off_p + (k >> 2) * (kM * 128) + (k & 3) * 32, 16),
-               desc_sw128(vb + k * 2048, kN * 128), id_pv, (t > 0 || k > 0) ? 1u : 0u);
-        umma_commit(v_empty + 8 * (t & 1));
-        umma_commit(pv_done + 8 * (t & 1));
+          umma_ts(tmem + 256 + x * 128, tmem + x * 128 + k * 8, desc_sw128(vb + k * 2048, kN * 128), id_pv,
+                  (t > 0 || k > 0) ? 1u : 0u);
+      };
+      mbar_wait(k_full, 0);
+      tc_fence_after();
+      for (int x = 0; x < nq; ++x) issue_s(x, 0);
+      umma_commit(k_empty);
+      for (int t = 0; t < n_tiles; ++t) {
+        const bool more = t + 1 < n_tiles;
+        mbar_wait(v_full + 8 * (t % kVStages), (t / kVStages) & 1);
+        if (more) mbar_wait(k_full + 8 * ((t + 1) % kKStages), ((t + 1) / kKStages) & 1);
+        for (int x = 0; x < nq; ++x) {
+          issue_pv(x, t);
+          if (x == nq - 1) umma_commit(v_empty + 8 * (t % kVStages));
+          if (more) {
+            issue_s(x, t + 1);  // in order after P_x(t) was read: S_x may overwrite P_x
+            if (x == nq - 1) umma_commit(k_empty + 8 * ((t + 1) % kKStages));
+          } else {
+            umma_commit(o_full + 8 * x);
+          }
+        }
       }
     }
   } else {
     // ================================ softmax ================================
-    const int quarter = warp & 3;           // TMEM lanes [32*quarter, 32*quarter + 32)
+    // warps 2..5 -> Q tile 0, warps 6..9 -> Q tile 1; thread = TMEM lane = MMA row
+    const int x = (warp - 2) >> 2;
+    const int quarter = warp & 3;           // TMEM lanes [32*quarter, 32*quarter + 32) (warp % 4 rule)
     const int row = quarter * 32 + lane;
     const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16);
+    const uint32_t s_col = x * 128, o_col = 256 + x * 128;
     const int g = p.group;
-    const int pos_idx = row / g;
+    const int pos_idx = x * bp + row / g;
     const bool valid = pos_idx < n_valid;
     const int prow = valid ? p0 + pos_idx : p0;  // causal limit of this row
-    float m_run = -INFINITY, l_run = 0.f;
-    uint8_t* prow_base = smem + LY::off_p + row * 128;
-    for (int t = 0; t < n_tiles; ++t) {
-      mbar_wait(s_full + 8 * (t & 1), (t >> 1) & 1);
-      tc_fence_after();
-      float x[kN];
-#pragma unroll
-      for (int c = 0; c < kN / 32; ++c) tmem_ld32(lane_addr + (t & 1) * 128 + c * 32, reinterpret_cast<uint32_t*>(x + 32 * c));
-      tmem_wait_ld();
-      const int lim = prow - t * kN;  // keys j <= lim of this tile are visible
-      if (!__all_sync(0xffffffffu, lim >= kN - 1)) {  // diagonal / last tiles only
-#pragma unroll
-        for (int j = 0; j < kN; ++j)
-          if (j > lim) x[j] = -INFINITY;
-      }
-      // row max of the raw scores with 8 independent chains (scale > 0 commutes with max)
-      float mx[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) mx[i] = x[i];
-#pragma unroll
-      for (int j = 8; j < kN; ++j) mx[j & 7] = fmaxf(mx[j & 7], x[j]);
-      const float m_tile =
-          fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) *
-          p.scale_log2;
-      // lazy rescale: a row moves its reference max only when the tile max exceeds it by more
-      // than the headroom; the TMEM round trip of O is warp-uniform (tcgen05.ld/st are .aligned)
-      // and needs P.V of tile t-1 complete
-      const bool grow = m_tile > m_run + kRescaleHeadroom;
-      if (t > 0 && __any_sync(0xffffffffu, grow)) {
-        mbar_wait(pv_done + 8 * ((t - 1) & 1), ((t - 1) >> 1) & 1);
-        const float alpha = grow ? ex2(m_run - m_tile) : 1.f;
-        l_run *= alpha;
+    if (x < nq) {
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int t = 0; t < n_tiles; ++t) {
+        // S_x(t) complete implies P_x(t-1).V(t-1) complete (commit order): O_x and P_x are free
+        mbar_wait(s_full + 8 * x, t & 1);
         tc_fence_after();
+        float xs[kN];
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t o[32];
-          tmem_ld32(lane_addr + 256 + c * 32, o);
-          tmem_wait_ld();
+        for (int c = 0; c < kN / 32; ++c) tmem_ld32(lane_addr + s_col + c * 32, reinterpret_cast<uint32_t*>(xs + 32 * c));
+        tmem_wait_ld();
+        const int lim = prow - t * kN;  // keys j <= lim of this tile are visible
+        if (!__all_sync(0xffffffffu, lim >= kN - 1)) {  // diagonal / last tiles only
 #pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-          tmem_st32(lane_addr + 256 + c * 32, o);
+          for (int j = 0; j < kN; ++j)
+            if (j > lim) xs[j] = -INFINITY;
+        }
+        float mx[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx[i] = xs[i];
+#pragma unroll
+        for (int j = 8; j < kN; ++j) mx[j & 7] = fmaxf(mx[j & 7], xs[j]);
+        const float m_tile =
+            fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) *
+            p.scale_log2;
+        // lazy rescale: the reference max moves only when the tile max exceeds it by more than
+        // the headroom; the TMEM round trip of O is warp-uniform (tcgen05.ld/st are .aligned)
+        const bool grow = m_tile > m_run + kRescaleHeadroom;
+        if (t > 0 && __any_sync(0xffffffffu, grow)) {
+          const float alpha = grow ? ex2(m_run - m_tile) : 1.f;
+          l_run *= alpha;
+#pragma unroll 1
+          for (int c = 0; c < D / 16; ++c) {  // 16 columns at a time: the 128 scores stay live
+            uint32_t o[16];
+            tmem_ld16(lane_addr + o_col + c * 16, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            tmem_st16(lane_addr + o_col + c * 16, o);
+          }
+        }
+        if (grow) m_run = m_tile;
+        float sm[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const float neg_m = -m_run;
+        // exponentials, packed to bf16 pairs and stored over S_x's first 64 columns 32 keys at a
+        // time (P_x: the A operand of P.V, read from TMEM)
+#pragma unroll
+        for (int c = 0; c < kN / 32; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const float a = ex2(fmaf(xs[32 * c + j], p.scale_log2, neg_m));
+            const float b = ex2(fmaf(xs[32 * c + j + 1], p.scale_log2, neg_m));
+            sm[j & 7] += a;
+            sm[(j + 1) & 7] += b;
+            pk[j / 2] = pack_bf16(a, b);
+          }
+          tmem_st16(lane_addr + s_col + c * 16, pk);
+        }
+        l_run += ((sm[0] + sm[1]) + (sm[2] + sm[3])) + ((sm[4] + sm[5]) + (sm[6] + sm[7]));
+        if (x == 0 && t == n_tiles - 1) {  // V rows past the last visible key may hold anything
+          const int need = last_key + 1 - t * kN;
+          if (row >= need) {
+            uint8_t* vrow = smem + LY::off_v + (t % kVStages) * LY::TILE + row * 128;
+#pragma unroll
+            for (int h = 0; h < HALVES; ++h)
+#pragma unroll
+              for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(vrow + h * kN * 128 + c * 16) = make_uint4(0, 0, 0, 0);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full + 8 * x);
       }
-      if (grow) m_run = m_tile;
-      float sm[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 independent partial sums
-      const float neg_m = -m_run;
+      // ---- epilogue: O_x / l -> bf16 -> out[q_row0 + pos][kvh*group + head][:] ----
+      mbar_wait(o_full + 8 * x, 0);
+      tc_fence_after();
+      const float inv = 1.f / l_run;
+      __nv_bfloat16* dst = p.out + (int64_t(q_row0 + pos_idx) * p.Hq + kvh * g + row % g) * D;
 #pragma unroll
-      for (int j = 0; j < kN; ++j) {  // exponentials first (in place), before the P-buffer wait
-        x[j] = ex2(fmaf(x[j], p.scale_log2, neg_m));
-        sm[j & 7] += x[j];
-      }
-      if (t >= 1) mbar_wait(pv_done + 8 * ((t - 1) & 1), ((t - 1) >> 1) & 1);  // P.V(t-1) read P
-      uint8_t* pbase = prow_base;
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t o[32];
+        tmem_ld32(lane_addr + o_col + c * 32, o);
+        tmem_wait_ld();
+        if (valid) {
 #pragma unroll
-      for (int c16 = 0; c16 < kN / 8; ++c16) {  // 16-byte chunk = 8 tokens
-        const float* pv = x + c16 * 8;
-        const int half = c16 >> 3, ch = c16 & 7;
-        uint4 v;
-        v.x = pack_bf16(pv[0], pv[1]);
-        v.y = pack_bf16(pv[2], pv[3]);
-        v.z = pack_bf16(pv[4], pv[5]);
-        v.w = pack_bf16(pv[6], pv[7]);
-        *reinterpret_cast<uint4*>(pbase + half * (kM * 128) + ((ch ^ (row & 7)) << 4)) = v;
-      }
-      l_run += ((sm[0] + sm[1]) + (sm[2] + sm[3])) + ((sm[4] + sm[5]) + (sm[6] + sm[7]));
-      if (t == n_tiles - 1) {  // V rows past the last visible key may hold anything: zero them
-        const int need = last_key + 1 - t * kN;
-        if (row >= need) {
-          uint8_t* vrow = smem + LY::off_v + (t & 1) * LY::TILE + row * 128;
-#pragma unroll
-          for (int h = 0; h < HALVES; ++h)
-#pragma unroll
-            for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(vrow + h * kN * 128 + c * 16) = make_uint4(0, 0, 0, 0);
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p_full + 8 * (t & 1));
-    }
-    // ---- epilogue: O / l -> bf16 -> out[q_row0 + pos][kvh*group + head][:] ----
-    mbar_wait(pv_done + 8 * ((n_tiles - 1) & 1), ((n_tiles - 1) >> 1) & 1);
-    tc_fence_after();
-    const float inv = 1.f / l_run;
-    __nv_bfloat16* dst = p.out + (int64_t(q_row0 + pos_idx) * p.Hq + kvh * g + row % g) * D;
-#pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t o[32];
-      tmem_ld32(lane_addr + 256 + c * 32, o);
-      tmem_wait_ld();
-      if (valid) {
-#pragma unroll
-        for (int e = 0; e < 32; e += 8) {
-          uint4 v;
-          v.x = pack_bf16(__uint_as_float(o[e + 0]) * inv, __uint_as_float(o[e + 1]) * inv);
-          v.y = pack_bf16(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
-          v.z = pack_bf16(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
-          v.w = pack_bf16(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
-          *reinterpret_cast<uint4*>(dst + c * 32 + e) = v;
+          for (int e = 0; e < 32; e += 8) {
+            uint4 v;
+            v.x = pack_bf16(__uint_as_float(o[e + 0]) * inv, __uint_as_float(o[e + 1]) * inv);
+            v.y = pack_bf16(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
+            v.z = pack_bf16(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
+            v.w = pack_bf16(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
+            *reinterpret_cast<uint4*>(dst + c * 32 + e) = v;
+          }
         }
       }
     }

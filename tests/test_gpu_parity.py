@@ -282,3 +282,24 @@ def test_map_units_follow_ownership():
     t.check_tables()
     t.check_bytes()
     t.attention(31, [0, 1])
+
+
+@pytest.mark.parametrize("dyn", ["0", "16"])
+def test_attention_is_deterministic(dyn, monkeypatch):
+    """DESIGN.md R17: a launch's output bits do not depend on which CTA claimed which work (the
+    merge order is fixed by record id) — repeated launches, with and without dynamic tickets,
+    give identical bits, and they are within R8 of the oracle."""
+    import torch
+    monkeypatch.setenv("ELLM_ATTN_DYN_DIV", dyn)
+    t = Twin(1, 32, 8, 128, 16, 1100, 1100, 4, 400, 0, seed=13)
+    lens = [6000, 77, 2900, 1234]  # 640 tiles >= 4 x #SM: the dynamic tail engages with dyn=16
+    assert t.reserve([0, 1, 2, 3], lens) == 0
+    t.append_all_layers([0, 1, 2, 3], lens)
+    rc, (first, _) = t.attention(0, [2, 0, 3, 1])
+    assert rc == 0
+    q = bits_to_torch(t.q_bits([2, 0, 3, 1], 0))
+    for _ in range(4):
+        out = torch.empty((4, 32, 128), dtype=torch.bfloat16, device="cuda")
+        assert t.p.attention(0, [2, 0, 3, 1], q, out, t.scale) == 0
+        torch.cuda.synchronize()
+        assert np.array_equal(torch_to_bits(out), first)
