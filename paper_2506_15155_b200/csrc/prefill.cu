@@ -21,6 +21,8 @@
 //    mask, base-2 online softmax with lazy rescaling (O in TMEM is rescaled only when the row max
 //    grows by more than 2^8), P written as bf16 into shared memory in the swizzled K-major layout,
 //    and at the end O / l -> bf16 -> global.
+#include <cstdlib>
+
 #include <cuda_bf16.h>
 
 #include "internal.h"
@@ -90,6 +92,18 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+// 2^x on the FMA / integer pipes (no MUFU): round-to-nearest split x = j + f, f in [-1/2, 1/2],
+// 2^f by a cubic (relative-error fit on [-1/2, 1/2]: < 7.5e-5, far below bf16's 2^-9 half-ulp
+// of P; checked in tests/test_prefill_exp2.py against numpy), then j added
+// to the exponent field. Inputs are clamped at -125 so the result stays a normal float (>= 2^-125.5;
+// masked scores, -inf, give that instead of 0 — 1e-38 of a zeroed or finite V row).
+__device__ __forceinline__ float ex2_fma(float x) {
+  x = fmaxf(x, -125.f);
+  const float r = x + 12582912.f;  // 1.5 * 2^23: the low mantissa bits of r hold round(x)
+  const float f = x - (r - 12582912.f);
+  const float q = fmaf(fmaf(fmaf(0.05517161f, f, 0.24261114f), f, 0.693261f), f, 0.99992807f);
+  return __int_as_float(__float_as_int(q) + (__float_as_int(r) << 23));
 }
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -199,7 +213,8 @@ struct PParams {
 // first 64 columns — and O_x at [256 + 128x, 256 + 128x + D). Both tiles share every K/V tile.
 // The MMA thread issues, per key tile t:  PV_0(t), S_0(t+1), PV_1(t), S_1(t+1), so while softmax
 // warpgroup x works on S_x(t+1) the tensor pipe runs the other tile's P.V and S.
-template <int D>
+// EMU: of every 8 softmax exponentials, this many run on the FMA pipe (ex2_fma), the rest on MUFU
+template <int D, int EMU>
 __global__ void __launch_bounds__(kThreads, 1)
     prefill_kernel(const __grid_constant__ PrefillMaps maps, const PParams p) {
   using LY = Layout<D>;
@@ -430,8 +445,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t pk[16];
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
-            const float a = ex2(fmaf(xs[32 * c + j], p.scale_log2, neg_m));
-            const float b = ex2(fmaf(xs[32 * c + j + 1], p.scale_log2, neg_m));
+            const float ya = fmaf(xs[32 * c + j], p.scale_log2, neg_m);
+            const float yb = fmaf(xs[32 * c + j + 1], p.scale_log2, neg_m);
+            const float a = (j & 7) < EMU ? ex2_fma(ya) : ex2(ya);
+            const float b = ((j + 1) & 7) < EMU ? ex2_fma(yb) : ex2(yb);
             sm[j & 7] += a;
             sm[(j + 1) & 7] += b;
             pk[j / 2] = pack_bf16(a, b);
@@ -487,17 +504,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int D>
-cudaError_t launch_d(const PrefillMaps& maps, const PParams& prm, int n_work, cudaStream_t s) {
+template <int D, int EMU>
+cudaError_t launch_de(const PrefillMaps& maps, const PParams& prm, int n_work, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(prefill_kernel<D, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Layout<D>::bytes);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  prefill_kernel<D><<<n_work, kThreads, Layout<D>::bytes, s>>>(maps, prm);
+  prefill_kernel<D, EMU><<<n_work, kThreads, Layout<D>::bytes, s>>>(maps, prm);
   return cudaGetLastError();
+}
+
+constexpr int kDefaultEmu = 2;
+template <int D>
+cudaError_t launch_d(const PrefillMaps& maps, const PParams& prm, int n_work, cudaStream_t s) {
+  const char* v = std::getenv("ELLM_PF_EMU");  // measurement knob: 0, 2, 3 or 4 of every 8
+  const int emu = v ? std::atoi(v) : kDefaultEmu;
+  switch (emu) {
+    case 0: return launch_de<D, 0>(maps, prm, n_work, s);
+    case 3: return launch_de<D, 3>(maps, prm, n_work, s);
+    case 4: return launch_de<D, 4>(maps, prm, n_work, s);
+    default: return launch_de<D, 2>(maps, prm, n_work, s);
+  }
 }
 
 }  // namespace
