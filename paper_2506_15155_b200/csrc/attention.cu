@@ -32,6 +32,14 @@
 namespace ellm {
 namespace {
 
+#ifndef ELLM_MERGE_DEPTH
+#define ELLM_MERGE_DEPTH 8   // record loads in flight per lane in the end-of-CTA merges
+#endif
+#ifndef ELLM_MERGE_ROW_UNROLL
+#define ELLM_MERGE_ROW_UNROLL 1
+#endif
+#define ELLM_PRAGMA_S(x) _Pragma(#x)
+#define ELLM_PRAGMA(x) ELLM_PRAGMA_S(x)
 constexpr int kConsumerWarps = 8;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 
@@ -139,6 +147,7 @@ struct Params {
   unsigned long long ticket_base;
   const int4* dyn_info;        // per unit: {vr, tile in vr, first-segment tiles, len}, {req, 0, 0, 0}
   const int32_t* dyn_ent;      // per unit: [U][npieces] chunk ids of its tiles (-1: none)
+  const int4* cta_first;       // per CTA: {vr, cum_s[vr], cum_s[vr+1], len}, {req, 0, 0, 0} of its first segment
   const __nv_bfloat16* q;
   __nv_bfloat16* out;
   const uint4* k_new;      // fused decode append: [n][Hkv][d] new token rows, or nullptr
@@ -169,7 +178,13 @@ struct Params {
   int32_t gscope_gpu;  // 1: gather release at gpu scope (measurement knob, single-device windows only)
   uint32_t* gdone;     // gather launches: CTAs finished (monotone counter) and this launch's final value
   uint32_t gdone_target;
+  unsigned long long* trace;  // ellm_set_attn_trace: [G][8] %globaltimer stamps of this launch, or null
 };
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 constexpr int kFirst = 1, kLast = 2, kDone = 4;  // stage metadata flags
 
 // LSE merge of the partial records of virtual request vr, run by the 256
@@ -196,23 +211,37 @@ __device__ __forceinline__ void merge_request(const Params& p, int vr, int rows,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int e4 = lane % LPR, sub = lane / LPR;
   const unsigned seg_mask = RPW == 1 ? 0xffffffffu : (0xffffu << (16 * sub));
+  ELLM_PRAGMA(unroll ELLM_MERGE_ROW_UNROLL)
   for (int row0 = (warp - w0) * RPW; row0 < rows; row0 += nw * RPW) {
     const int row = row0 + sub;
     const bool live = row < rows;
-    float M = -INFINITY;
-    for (int64_t k = e4; live && k < P; k += LPR) M = fmaxf(M, __ldcg(p.part_ml + (pid(k) * rows + row) * 2));
-#pragma unroll
-    for (int o = LPR / 2; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(seg_mask, M, o));
-    float L = 0.f;
+    // one pass over the records in chunks of LPR (usually one chunk): lane e4 loads record
+    // base+e4's (m, l) — the chunk's max and weights need no second load — then the o rows in
+    // batches of DEPTH independent loads; a later chunk with a larger max rescales what is
+    // accumulated (same LSE rule). Round trips to L2: 1 + ceil(P / DEPTH) instead of
+    // 2 + ceil(P / DEPTH) plus a separate max pass.
+    float M = -INFINITY, L = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int64_t base = 0; base < P; base += LPR) {
-      float my_w = 0.f;
       const int64_t mk = base + e4;
-      if (live && mk < P) {
-        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.part_ml + (pid(mk) * rows + row) * 2));
-        my_w = ex2(ml.x - M);  // a record with no valid token has m = -inf -> weight 0
-        L += my_w * ml.y;
+      float2 ml = make_float2(-INFINITY, 0.f);
+      if (live && mk < P) ml = __ldcg(reinterpret_cast<const float2*>(p.part_ml + (pid(mk) * rows + row) * 2));
+      float cm = ml.x;
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(seg_mask, cm, o));
+      const float Mn = fmaxf(M, cm);
+      if (Mn > M && M != -INFINITY) {  // a later chunk raised the max: rescale (segment-uniform)
+        const float sc = ex2(M - Mn);
+        L *= sc;
+        acc.x *= sc;
+        acc.y *= sc;
+        acc.z *= sc;
+        acc.w *= sc;
       }
+      M = Mn;
+      // a record with no valid token has m = -inf -> weight 0 (and so does every lane past P)
+      const float my_w = (M == -INFINITY || ml.x == -INFINITY) ? 0.f : ex2(ml.x - M);
+      L += my_w * ml.y;
       const int cnt = int(min(int64_t(LPR), P - base));
       for (int j0 = 0; j0 < cnt; j0 += DEPTH) {  // DEPTH independent record loads in flight
         float4 ov[DEPTH];
@@ -274,22 +303,6 @@ __device__ __noinline__ void gather_flag_spin(const uint32_t* flag, uint32_t tar
   }
 }
 
-// The largest vr with cum[vr] <= t (cum non-decreasing, cum[0] = 0 <= t), found by the whole
-// warp: each round the 32 lanes probe evenly spaced entries and the bracket shrinks 32x, so a
-// CTA's first lookup costs ceil(log32 n_vr) dependent loads instead of log2 n_vr (launch ramp).
-__device__ __forceinline__ int find_vr(const int32_t* cum, int n_vr, int64_t t) {
-  const int lane = threadIdx.x & 31;
-  int lo = 0, hi = n_vr;  // answer in [lo, hi)
-  while (hi - lo > 1) {
-    const int step = (hi - lo + 31) >> 5;
-    const int idx = lo + lane * step;
-    const unsigned le = __ballot_sync(0xffffffffu, idx < hi && __ldg(cum + idx) <= t);
-    lo += (31 - __clz(le)) * step;  // lane 0 always qualifies (cum[lo] <= t)
-    hi = min(hi, lo + step);
-  }
-  return lo;
-}
-
 template <int D, int HB>
 __global__ void __launch_bounds__(kThreads, 1)
     paged_attn_kernel(const __grid_constant__ CUtensorMap tmap, const Params p) {
@@ -318,6 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t qfull0 = smem_u32(bars + 2 * NST), qempty0 = smem_u32(bars + 2 * NST + kQSlots);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 8 + 0] = gtimer();
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(full0 + 8 * s, 1);
@@ -384,6 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto pdl_wait = [&]() {
       if (!waited) {
         asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (p.trace && lane == 0) p.trace[blockIdx.x * 8 + 1] = gtimer();
         if (p.wait_flag != nullptr) {  // folded a10 wait: every rank's rows of the previous layer
           if (lane == 0) gather_flag_spin(p.wait_flag, p.wait_target, p.wait_timeout_ns);
           __syncwarp();
@@ -392,22 +407,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         waited = true;
       }
     };
+    // the first static segment comes from the host-built per-CTA record (one load, no search)
+    const int4 cf0 = __ldg(p.cta_first + 2 * b), cf1 = __ldg(p.cta_first + 2 * b + 1);
+    bool first_static = true;
     for (;;) {
-      int vr = dyn ? uinfo.x : find_vr(cum, p.n_vr, t_begin);
+      int vr = dyn ? uinfo.x : cf0.x;
       for (int64_t tile = t_begin; tile < t_end; ++vr) {
         const bool first_dyn_seg = dyn && tile == t_begin;  // everything known from uinfo
-        const int64_t seg_end =
-            first_dyn_seg ? min(t_end, t_begin + uinfo.z) : min(t_end, int64_t(__ldg(cum + vr + 1)));
+        const bool fs = first_static;                         // everything known from cf0 / cf1
+        first_static = false;
+        const int64_t seg_end = first_dyn_seg ? min(t_end, t_begin + uinfo.z)
+                                : fs          ? min(t_end, int64_t(cf0.z))
+                                              : min(t_end, int64_t(__ldg(cum + vr + 1)));
         // a request with no tiles in this space (a short request's empty dynamic tail) is not a
         // segment: staging its Q would leave a Q slot no consumer releases
         if (seg_end <= tile) continue;
         const int ireq = vr / p.HG, hg = vr % p.HG;
-        const int32_t len = first_dyn_seg ? uinfo.w : __ldg(p.len + ireq);
+        const int32_t len = first_dyn_seg ? uinfo.w : fs ? cf0.w : __ldg(p.len + ireq);
         const int32_t* trow =
-            p.table + int64_t(first_dyn_seg ? uinfo2.x : __ldg(p.req + ireq)) * p.table_stride;
+            p.table + int64_t(first_dyn_seg ? uinfo2.x : fs ? cf1.x : __ldg(p.req + ireq)) * p.table_stride;
         // space coordinate of the request's first tile in this space, minus its tile offset
         const int64_t tile0 =
             first_dyn_seg ? t_begin - uinfo.y
+            : fs          ? int64_t(cf0.y)
                           : __ldg(cum + vr) - (dyn ? int64_t(__ldg(p.cum_s + vr + 1) - __ldg(p.cum_s + vr)) : 0);
         const int qs = int(segc % kQSlots);
         auto stage_q = [&]() {
@@ -574,8 +596,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   float o[NT][4];
   float m_run = -INFINITY, l_run = 0.f;
   int32_t len = 0;
+  bool first_data = true;
   for (;;) {
     mbar_wait(full0 + 8 * stage, phase);
+    if (p.trace && threadIdx.x == 0 && first_data) p.trace[blockIdx.x * 8 + 2] = gtimer();
+    first_data = false;
     const int4 meta = s_meta[stage];
     if (meta.w & kDone) break;
     const int vr = meta.x;
@@ -675,16 +700,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty0 + 8 * stage);
+    const bool seg_last = (meta.w & kLast) != 0;
+    // with NSUB > 1 subtile warps per head, a segment's last stage doubles as the scratch of the
+    // in-CTA combine below: it is released only after that
+    const uint32_t cur_stage = uint32_t(stage);
+    if (lane == 0 && !(seg_last && NSUB > 1)) mbar_arrive(empty0 + 8 * stage);
     if (++stage == NST) { stage = 0; phase ^= 1; }
-    if (!(meta.w & kLast)) continue;
+    if (!seg_last) continue;
 
-    // ---- partial record of (owner, virtual request vr, subtile slot j) ----
+    // ---- partial record of (owner, virtual request vr): one per q-head row ----
     float l_tot = l_run + __shfl_xor_sync(0xffffffffu, l_run, 1);
     l_tot += __shfl_xor_sync(0xffffffffu, l_tot, 2);
-    if (g < p.group) {
-      const int64_t rec = (int64_t(meta.z) * NSUB + j) * rows + row;
-      float* dst = p.part + rec * D;
+    // this lane's o fragment as 16-byte pieces: piece k of the row at float offset foff(k)
+    auto write_frag = [&](float* dst) {
       if constexpr (D == 128) {
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
@@ -702,7 +730,54 @@ __global__ void __launch_bounds__(kThreads, 1)
         c[0] = make_float4(o[0][1], o[1][1], o[2][1], o[3][1]);
         c[1] = make_float4(o[4][1], o[5][1], o[6][1], o[7][1]);
       }
-      if (q == 0) *reinterpret_cast<float2*>(p.part_ml + rec * 2) = make_float2(m_run, l_tot);
+    };
+    if constexpr (NSUB == 1) {
+      if (g < p.group) {
+        const int64_t rec = int64_t(meta.z) * rows + row;
+        write_frag(p.part + rec * D);
+        if (q == 0) *reinterpret_cast<float2*>(p.part_ml + rec * 2) = make_float2(m_run, l_tot);
+      }
+    } else {
+      // In-CTA combine of the NSUB subtile partials of each q-head row (same LSE rule as the
+      // merge), so a segment leaves ONE record per row instead of NSUB: the end-of-launch merges
+      // then read NSUB times fewer records (measured at the 8-way C4 shard, NSUB = 8: ~26 -> ~3
+      // records per request; the merge is on the launch's critical path). Scratch: the stage
+      // just consumed, [NSUB][rows][D] fp32 + [NSUB][rows] (m, l), at most 32 KiB + 512 B.
+      float* scr = reinterpret_cast<float*>(smem + cur_stage * SB);
+      float* scr_ml = scr + NSUB * rows * D;
+      asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");  // every warp's K/V reads done
+      if (g < p.group) {
+        write_frag(scr + (j * rows + row) * D);
+        if (q == 0) *reinterpret_cast<float2*>(scr_ml + (j * rows + row) * 2) = make_float2(m_run, l_tot);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+      constexpr int LPR = D / 4, RPW = 32 / LPR;
+      const int e4 = lane % LPR, sub = lane / LPR;
+      for (int r = warp * RPW + sub; r < rows; r += kConsumerWarps * RPW) {
+        float M = -INFINITY;
+#pragma unroll
+        for (int jj = 0; jj < NSUB; ++jj) M = fmaxf(M, scr_ml[(jj * rows + r) * 2]);
+        float L = 0.f;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int jj = 0; jj < NSUB; ++jj) {
+          const float2 ml = *reinterpret_cast<const float2*>(scr_ml + (jj * rows + r) * 2);
+          const float w = ml.x == -INFINITY ? 0.f : ex2(ml.x - M);  // an empty subtile: weight 0
+          const float4 v = reinterpret_cast<const float4*>(scr + (jj * rows + r) * D)[e4];
+          L += w * ml.y;
+          acc.x += w * v.x;
+          acc.y += w * v.y;
+          acc.z += w * v.z;
+          acc.w += w * v.w;
+        }
+        const int64_t rec = int64_t(meta.z) * rows + r;
+        reinterpret_cast<float4*>(p.part + rec * D)[e4] = acc;
+        if (e4 == 0) *reinterpret_cast<float2*>(p.part_ml + rec * 2) = make_float2(M, L);
+      }
+      // generic-proxy use of the stage is over before the TMA (async proxy) refills it
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+      if (lane == 0) mbar_arrive(empty0 + 8 * cur_stage);
     }
     // ---- arrival: the owner that completes request vr's count merges it (a5, fused) ----
     // bar.sync orders every consumer's record stores before thread 0's gpu-scope fence +
@@ -725,15 +800,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (__shfl_sync(0xffffffffu, now, 0)) {
-        merge_request<D, 1>(p, vr, rows, NSUB, HB, 0, 1);
+        merge_request<D, 1>(p, vr, rows, 1, HB, 0, 1);
         if (lane == 0) ++s_n_now;
       }
     }
   }
   // ---- end of this CTA's work: all consumer warps merge the requests it completed ----
+  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 8 + 3] = gtimer();
   asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
   __threadfence();
-  for (int k = 0; k < s_n_merge; ++k) merge_request<D, 8>(p, s_merge[k], rows, NSUB, HB, 0, kConsumerWarps);
+  for (int k = 0; k < s_n_merge; ++k)
+    merge_request<D, ELLM_MERGE_DEPTH>(p, s_merge[k], rows, 1, HB, 0, kConsumerWarps);
+  if (p.trace && threadIdx.x == 0) {
+    p.trace[blockIdx.x * 8 + 4] = gtimer();
+    p.trace[blockIdx.x * 8 + 6] = (unsigned long long)(s_n_merge + s_n_now);
+  }
   if (p.n_peer > 0) {
     // a10 signal. Every CTA orders its row stores before a gpu-scope count (the named barrier
     // gathers the consumer threads' stores at thread 0, whose acq_rel fence + relaxed add is a
@@ -760,6 +841,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 8 + 5] = gtimer();
 }
 
 template <int D, int HB>
@@ -840,6 +922,7 @@ cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh,
   prm.ticket_base = plan.ticket_base;
   prm.dyn_info = reinterpret_cast<const int4*>(plan.dyn_info);
   prm.dyn_ent = plan.dyn_ent;
+  prm.cta_first = reinterpret_cast<const int4*>(plan.cta_first);
   prm.q = static_cast<const __nv_bfloat16*>(q);
   prm.out = static_cast<__nv_bfloat16*>(out);
   prm.k_new = static_cast<const uint4*>(plan.k_new);
@@ -873,6 +956,7 @@ cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh,
     prm.gflag[i] = plan.gflag[i];
   }
   prm.gdone = plan.gdone;
+  prm.trace = plan.trace;
   prm.gdone_target = plan.gdone_target;
   prm.wait_flag = plan.wait_flag;
   prm.wait_target = plan.wait_target;

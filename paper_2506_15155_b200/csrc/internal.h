@@ -155,6 +155,7 @@ struct AttnPlan {
   unsigned long long ticket_base = 0;
   const int32_t* dyn_info = nullptr;  // device: [n_dyn][8] (int4 pairs, see attention.cu Params)
   const int32_t* dyn_ent = nullptr;   // device: [n_dyn][U * npieces]
+  const int32_t* cta_first = nullptr; // device: [G][8] first static segment of each CTA
   // fused decode append (ellm_decode_append_attention): one new token per request, or nullptr
   const void* k_new = nullptr;
   const void* v_new = nullptr;
@@ -166,6 +167,7 @@ struct AttnPlan {
   uint32_t* gflag[kMaxPeers] = {};
   int32_t n_peer = 0, Hq_out = 0, q_off = 0;
   uint32_t* gdone = nullptr;   // CTAs of gather launches that finished (device counter)
+  unsigned long long* trace = nullptr;  // ellm_set_attn_trace slot of this launch
   uint32_t gdone_target = 0;   // value the counter reaches when this launch's last CTA arrives
   // a10 folded gather wait (ellm_gather_wait_next): before staging Q or writing anything, the
   // producer spins (acquire, system scope) until *wait_flag reaches wait_target; nullptr = none
@@ -269,6 +271,7 @@ struct ellm_pool {
   std::vector<int32_t> cache_key;     // req ids then lens
   uint64_t table_epoch = 0;           // bumped by every table entry change
   int64_t cache_info_off = 0, cache_ent_off = 0;  // dynamic-unit arrays inside the descriptor
+  int64_t cache_cta_off = 0;        // per-CTA first-segment info in the cached descriptor
   uint64_t cache_epoch = ~uint64_t(0);
   const int32_t* cache_dev = nullptr;
   uint64_t cache_gen = 0;
@@ -277,6 +280,9 @@ struct ellm_pool {
   unsigned long long* d_ticket = nullptr;  // dynamic-unit ticket counter (device)
   uint64_t ticket_base = 0;                // tickets consumed by earlier launches
   uint32_t gdone_base = 0;                 // gather-launch CTAs counted by earlier launches
+  unsigned long long* trace_buf = nullptr; // ellm_set_attn_trace: caller's device buffer
+  int32_t trace_slots = 0;
+  int64_t trace_launch = 0;
   int64_t dyn_div = 0;                     // dynamic tail = tiles/dyn_div per request (0: static only)
   int64_t dyn_unit = 8;                    // minimum tiles per dynamic unit
 

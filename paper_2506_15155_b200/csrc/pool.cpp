@@ -398,6 +398,15 @@ const char* ellm_status_string(int s) {
 int ellm_last_cuda_error(const ellm_pool* p) { return p ? p->last_cuda_error : 0; }
 int64_t ellm_kernel_launches(const ellm_pool* p) { return p ? p->launches : 0; }
 
+int ellm_set_attn_trace(ellm_pool* p, void* device_buf, int32_t launches) {
+  if (!p || launches < 0 || (device_buf && launches == 0)) return ELLM_ERR_INVALID_ARG;
+  if (!p->has_dev) return ELLM_ERR_NO_DEVICE;
+  p->trace_buf = static_cast<unsigned long long*>(device_buf);
+  p->trace_slots = device_buf ? launches : 0;
+  p->trace_launch = 0;
+  return ELLM_OK;
+}
+
 // Split-K state of the attention launches, sized for calls of up to `reqs` list entries
 // (duplicates allowed, so a call may list more than max_requests): partial records
 // pid < (G + 2 n_vr + n_dyn) * nsub, each [HB*group][D] fp32 + (m, l), and one arrival counter
@@ -1015,6 +1024,26 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
         }
       }
     }
+    // Per CTA, its first static segment as the producer would look it up (a warp-wide search of
+    // cum_s, then len / req / cum loads: three dependent L2 round trips before the first TMA):
+    // {vr, cum_s[vr], cum_s[vr + 1], len}, {req, 0, 0, 0}.
+    p->cache_cta_off = (int64_t(d.size()) + 3) & ~int64_t(3);
+    d.resize(size_t(p->cache_cta_off + 8 * int64_t(pl.G)), 0);
+    cum_s = d.data() + 2 * n;
+    {
+      int32_t v = 0;
+      for (int64_t b = 0; b < pl.G; ++b) {
+        const int64_t t0 = b * pl.W_s / pl.G;
+        while (v + 1 < n_vr && cum_s[v + 1] <= t0) ++v;
+        int32_t* ci = d.data() + p->cache_cta_off + 8 * b;
+        const int32_t r = reqs[v / a.HG];
+        ci[0] = v;
+        ci[1] = cum_s[v];
+        ci[2] = cum_s[v + 1];
+        ci[3] = int32_t(p->len[size_t(r)]);
+        ci[4] = r;
+      }
+    }
     const int32_t* dd;
     uint64_t gen;
     if (d.size() * 4 > p->ring.seg_bytes()) return ELLM_ERR_UNSUPPORTED;
@@ -1035,6 +1064,7 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
   AttnPlan plan = p->cache_plan;
   plan.dyn_info = dd + p->cache_info_off;
   plan.dyn_ent = dd + p->cache_ent_off;
+  plan.cta_first = dd + p->cache_cta_off;
   plan.ticket = p->d_ticket;
   plan.ticket_base = p->ticket_base;
   plan.k_new = k_new;
@@ -1052,6 +1082,10 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
     // the CTA that finishes last (gpu-scope count, monotone across launches) signals every rank
     plan.gdone = reinterpret_cast<uint32_t*>(p->d_ticket + 1);
     plan.gdone_target = p->gdone_base + uint32_t(plan.G);
+  }
+  if (p->trace_buf) {  // ellm_set_attn_trace: this launch's [G][8] slot
+    plan.trace = p->trace_buf + (p->trace_launch % p->trace_slots) * int64_t(p->num_sms) * 8;
+    ++p->trace_launch;
   }
   if (p->g_wait_flag) {  // a folded gather wait (ellm_gather_wait_next) is consumed by this launch
     plan.wait_flag = p->g_wait_flag;

@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libellm.so")
+# ELLM_LIB_PATH: another in-tree build of the same sources (A/B measurements of build variants)
+LIB_PATH = os.environ.get("ELLM_LIB_PATH") or os.path.join(_HERE, "libellm.so")
 
 OK = 0
 ERR = {
@@ -101,6 +102,7 @@ _SIGS = {
     "ellm_attention_gather": (ctypes.c_int, [_P, _I32, _I32, _P, _V, _V, _V, _I64, ctypes.c_float, _V]),
     "ellm_gather_wait": (ctypes.c_int, [_P, _I32, _V]),
     "ellm_gather_wait_next": (ctypes.c_int, [_P, _I32]),
+    "ellm_set_attn_trace": (ctypes.c_int, [_P, _V, _I32]),
     "ellm_memcpy_async": (ctypes.c_int, [_V, _V, _I64, _V]),
     "ellm_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "ellm_last_cuda_error": (ctypes.c_int, [_P]),
@@ -223,6 +225,10 @@ class Pool:
 
     def gather_wait(self, layer, stream=None) -> int:
         return ellm_gather_wait(self._h, int(layer), _sptr(stream))
+
+    def set_attn_trace(self, device_buf, launches: int) -> int:
+        """Per-CTA timeline stamps of the next attention launches (profiling)."""
+        return ellm_set_attn_trace(self._h, _dptr(device_buf) if device_buf is not None else None, int(launches))
 
     def gather_wait_next(self, layer) -> int:
         """Fold the wait for `layer`'s gather into this pool's next attention launch."""
