@@ -398,7 +398,7 @@ int64_t ellm_kernel_launches(const ellm_pool* pool);
  * caller-owned device buffer of launches * #SM * 8 uint64, attention launch k of this pool
  * (counted from this call) writes, per CTA b, into slot (k % launches): [b*8 + 0] start,
  * [1] producer past griddepcontrol.wait, [2] first stage data seen, [3] streaming done,
- * [4] merges done, [5] end, all %globaltimer ns (0 = not reached), [6] requests merged.
+ * [4] merges done, [5] end, all %globaltimer ns (0 = not reached), [6] requests merged, [7] SM id.
  * NULL disables. launches < 0 or (buffer with launches == 0) -> INVALID_ARG. */
 int ellm_set_attn_trace(ellm_pool* pool, void* device_buf, int32_t launches);
 

@@ -179,6 +179,7 @@ struct Params {
   uint32_t* gdone;     // gather launches: CTAs finished (monotone counter) and this launch's final value
   uint32_t gdone_target;
   unsigned long long* trace;  // ellm_set_attn_trace: [G][8] %globaltimer stamps of this launch, or null
+  uint32_t range_shift;       // measurement knob: CTA i streams static range (i + shift) % G
 };
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -331,7 +332,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t qfull0 = smem_u32(bars + 2 * NST), qempty0 = smem_u32(bars + 2 * NST + kQSlots);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 8 + 0] = gtimer();
+  if (p.trace && threadIdx.x == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    p.trace[blockIdx.x * 8 + 0] = gtimer();
+    p.trace[blockIdx.x * 8 + 7] = smid;
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(full0 + 8 * s, 1);
@@ -352,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
 
-  const int b = blockIdx.x;
+  const int b = p.range_shift ? int((blockIdx.x + p.range_shift) % uint32_t(p.G)) : int(blockIdx.x);
   const int tok_box = p.T < TT ? p.T : TT;
   const int npieces = TT / tok_box;
   const int piece_bytes = 2 * HB * tok_box * D * 2;
@@ -370,7 +376,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // counter (the next ticket is requested before the current unit is streamed, hiding the
     // atomic's latency). `owner` names the partial records a range produces: record of
     // (owner, vr) = owner + vr, unique along the monotone staircase of (owner, request) pairs.
-    int64_t t_begin = int64_t(b) * p.W_s / p.G, t_end = int64_t(b + 1) * p.W_s / p.G;
+    // the first static segment and the static range come from the host-built per-CTA record
+    const int4 cf0 = __ldg(p.cta_first + 2 * b), cf1 = __ldg(p.cta_first + 2 * b + 1);
+    int64_t t_begin = cf1.y, t_end = cf1.z;
     int owner = b;
     const int32_t* cum = p.cum_s;
     // Dynamic units: two tickets stay outstanding (current + next), and the next unit's
@@ -407,8 +415,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         waited = true;
       }
     };
-    // the first static segment comes from the host-built per-CTA record (one load, no search)
-    const int4 cf0 = __ldg(p.cta_first + 2 * b), cf1 = __ldg(p.cta_first + 2 * b + 1);
     bool first_static = true;
     for (;;) {
       int vr = dyn ? uinfo.x : cf0.x;
@@ -957,6 +963,7 @@ cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh,
   }
   prm.gdone = plan.gdone;
   prm.trace = plan.trace;
+  prm.range_shift = plan.range_shift;
   prm.gdone_target = plan.gdone_target;
   prm.wait_flag = plan.wait_flag;
   prm.wait_target = plan.wait_target;

@@ -168,6 +168,7 @@ struct AttnPlan {
   int32_t n_peer = 0, Hq_out = 0, q_off = 0;
   uint32_t* gdone = nullptr;   // CTAs of gather launches that finished (device counter)
   unsigned long long* trace = nullptr;  // ellm_set_attn_trace slot of this launch
+  uint32_t range_shift = 0;    // ELLM_ATTN_RANGE_ROT=1: rotate static ranges over CTAs per launch
   uint32_t gdone_target = 0;   // value the counter reaches when this launch's last CTA arrives
   // a10 folded gather wait (ellm_gather_wait_next): before staging Q or writing anything, the
   // producer spins (acquire, system scope) until *wait_flag reaches wait_target; nullptr = none

@@ -972,10 +972,15 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
     pl.G = int32_t(std::min<int64_t>(p->num_sms, Ws));
     pl.U = Wd ? std::max<int64_t>(p->dyn_unit, (Wd + kMaxDynUnits - 1) / kMaxDynUnits) : 1;
     pl.n_dyn = Wd ? (Wd + pl.U - 1) / pl.U : 0;
-    // Static CTA b owns [floor(b W_s / G), floor((b+1) W_s / G)) of the static space; the CTA
-    // holding tile t is floor(((t+1) G - 1) / W_s). Dynamic unit u owns [u U, (u+1) U).
+    // Static CTA b owns [B[b], B[b+1]) = [floor(b W_s / G), floor((b+1) W_s / G)) of the static
+    // space (equal shares; the kernel reads its range from its per-CTA record). Dynamic unit u
+    // owns [u U, (u+1) U).
     const int64_t G = pl.G;
-    auto cta_of = [&](int64_t t) { return int32_t(((t + 1) * G - 1) / Ws); };
+    std::vector<int64_t> B(size_t(G) + 1);
+    for (int64_t b = 0; b <= G; ++b) B[size_t(b)] = b * Ws / G;
+    auto cta_of = [&](int64_t t) {  // the CTA holding static tile t
+      return int32_t(std::upper_bound(B.begin(), B.end(), t) - B.begin()) - 1;
+    };
     int32_t* bf = cum_d + n_vr + 1;
     int32_t* bl = bf + n_vr;
     int32_t* uf = bl + n_vr;
@@ -1033,7 +1038,7 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
     {
       int32_t v = 0;
       for (int64_t b = 0; b < pl.G; ++b) {
-        const int64_t t0 = b * pl.W_s / pl.G;
+        const int64_t t0 = B[size_t(b)];
         while (v + 1 < n_vr && cum_s[v + 1] <= t0) ++v;
         int32_t* ci = d.data() + p->cache_cta_off + 8 * b;
         const int32_t r = reqs[v / a.HG];
@@ -1042,6 +1047,8 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
         ci[2] = cum_s[v + 1];
         ci[3] = int32_t(p->len[size_t(r)]);
         ci[4] = r;
+        ci[5] = int32_t(B[size_t(b)]);      // static range [t_begin, t_end)
+        ci[6] = int32_t(B[size_t(b) + 1]);
       }
     }
     const int32_t* dd;
@@ -1082,6 +1089,13 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
     // the CTA that finishes last (gpu-scope count, monotone across launches) signals every rank
     plan.gdone = reinterpret_cast<uint32_t*>(p->d_ticket + 1);
     plan.gdone_target = p->gdone_base + uint32_t(plan.G);
+  }
+  {
+    static const bool rot_ranges = [] {
+      const char* v = std::getenv("ELLM_ATTN_RANGE_ROT");
+      return v && std::atoi(v) != 0;
+    }();
+    if (rot_ranges) plan.range_shift = uint32_t((p->trace_launch * 37 + 11) % std::max<int32_t>(1, plan.G));
   }
   if (p->trace_buf) {  // ellm_set_attn_trace: this launch's [G][8] slot
     plan.trace = p->trace_buf + (p->trace_launch % p->trace_slots) * int64_t(p->num_sms) * 8;

@@ -29,7 +29,7 @@ def main():
     L, B = wl.n_layers, wl.batch
     reqs, ones = list(range(B)), [1] * B
     lens = np.full(B, wl.context, np.int64)
-    steps, warm = 2, 2
+    steps, warm = 2, 4
     ins = [W.decode_inputs(wl, s, lens + s) for s in range(warm + steps)]
     out = torch.empty((L, B, wl.hq_local, wl.head_dim), dtype=torch.bfloat16, device="cuda")
     pg = shard.PeerGather(pool, 1, 0, wl.hq_local, L, B, wl.head_dim, device=0) if mode == "p2p" else None
@@ -75,6 +75,28 @@ def main():
     for k in keys:
         vals = [r[k] for r in rows if k in r]
         print(f"  {k:16s} {statistics.median(vals):8.2f}   (min {min(vals):7.2f}, max {max(vals):7.2f})")
+    # is a CTA's streaming time a property of its SM? per SM id: mean over launches of
+    # (streaming end - first data) relative to the launch median; correlation of two halves
+    dur = {}
+    for i in range(t.shape[0]):
+        x = t[i]
+        d = (x[:, 3] - x[:, 2]).astype(np.float64)
+        d /= np.median(d)
+        for c in range(x.shape[0]):
+            dur.setdefault(int(x[c, 7]), []).append(d[c])
+    sms = sorted(dur)
+    a = np.array([np.mean(dur[s][0::2]) for s in sms])
+    b = np.array([np.mean(dur[s][1::2]) for s in sms])
+    print(f"  per-SM streaming time / launch median: min {a.min():.3f} max {a.max():.3f}; "
+          f"even/odd-launch correlation {np.corrcoef(a, b)[0, 1]:.3f}")
+    same = np.mean([np.mean(t[i][:, 7] == t[0][:, 7]) for i in range(t.shape[0])])
+    print(f"  CTA -> SM mapping equal to the first traced launch's: {same:.3f} of CTAs on average")
+    bdur = np.array([(t[i][:, 3] - t[i][:, 2]) / np.median(t[i][:, 3] - t[i][:, 2]) for i in range(t.shape[0])])
+    ba, bb = bdur[0::2].mean(0), bdur[1::2].mean(0)
+    print(f"  per-CTA (blockIdx) streaming time ratio: min {ba.min():.3f} max {ba.max():.3f}; "
+          f"even/odd correlation {np.corrcoef(ba, bb)[0, 1]:.3f}")
+    slow = sorted(zip(((a + b) / 2).round(3), sms))[-6:]
+    print("  slowest SMs (ratio, smid):", slow)
     if pg is not None:
         pg.close()
     pool.close()
