@@ -438,7 +438,10 @@ def main():
             "frac": round(achieved / peak, 4), "traffic": traffic,
             "kernel": ("paged_attn_kernel: one ellm_decode_append_attention launch per layer (new-token "
                        "K/V append + attention + fused split-K merge)"),
-            "alg_bytes_per_launch": int(alg_bytes), "launch_ms": round(attn_mean, 4), "peak_source": peak_src}
+            "alg_bytes_per_launch": int(alg_bytes), "launch_ms": round(attn_mean, 4), "peak_source": peak_src,
+            "traffic_source": ("stored: dram__bytes_read.sum + dram__bytes_write.sum of one launch from the "
+                               "committed ncu --set full capture (profiles/attn_traffic.json, same workload); "
+                               "not measured in this run") if traffic is not None else None}
 
     # ---- end to end through host buffers: H2D of each step's inputs, D2H of its outputs ----
     e2e = None
