@@ -43,9 +43,11 @@ def parse():
                          "c5: 256-request prefill/decode churn with offload, compaction, shrink/grow")
     ap.add_argument("--swap-every", type=int, default=48,
                     help="c3: decode steps per offload/fetch round")
-    ap.add_argument("--swap-mode", choices=["sm", "ce", "mixed", "staged"], default="ce",
-                    help="c3: swap with the SM copy kernels, the DMA copy engines, or copy engines for "
-                         "swap-out and SM kernels for swap-in (mixed)")
+    ap.add_argument("--swap-mode", choices=["sm", "ce", "mixed", "staged"], default="staged",
+                    help="c3: swap with the SM copy kernels, the DMA copy engines, copy engines for "
+                         "swap-out and SM kernels for swap-in (mixed), or copy engines with a staged "
+                         "swap-in (host link -> staging buffer -> SM copy; the default: least "
+                         "interference with the decode, DESIGN.md §5 C3)")
     ap.add_argument("--resident", type=int, default=0,
                     help="c3: requests decoding in HBM (0 = as many as fit beside one in flight)")
     ap.add_argument("--gather", choices=["p2p", "nccl"], default="p2p",

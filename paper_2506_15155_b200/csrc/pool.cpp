@@ -98,7 +98,17 @@ struct CopyPiece {
   const uint8_t* s;
   int64_t n;
 };
+// ELLM_CE_MAX_COPY (bytes, measurement knob; 0 = unlimited): split contiguous runs into copies of
+// at most this size (C3 swap-in interference study).
+static int64_t ce_max_copy() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("ELLM_CE_MAX_COPY");
+    return e ? std::max<int64_t>(0, std::atoll(e)) : int64_t(0);
+  }();
+  return v;
+}
 cudaError_t issue_copies(const std::vector<CopyPiece>& pc, cudaStream_t stream) {
+  const int64_t cap = ce_max_copy();
   size_t i = 0;
   while (i < pc.size()) {
     const CopyPiece& a = pc[i];
@@ -108,9 +118,13 @@ cudaError_t issue_copies(const std::vector<CopyPiece>& pc, cudaStream_t stream) 
       while (j < pc.size() && pc[j].n == a.n && pc[j].d - pc[j - 1].d == dp && pc[j].s - pc[j - 1].s == sp) ++j;
       const size_t rows = j - i;
       cudaError_t e;
-      if (dp == a.n && sp == a.n)
-        e = cudaMemcpyAsync(a.d, a.s, size_t(a.n) * rows, cudaMemcpyDefault, stream);
-      else
+      if (dp == a.n && sp == a.n) {
+        const int64_t total = a.n * int64_t(rows);
+        const int64_t step = cap > 0 ? std::max<int64_t>(a.n, cap / a.n * a.n) : total;
+        e = cudaSuccess;
+        for (int64_t off = 0; off < total && e == cudaSuccess; off += step)
+          e = cudaMemcpyAsync(a.d + off, a.s + off, size_t(std::min(step, total - off)), cudaMemcpyDefault, stream);
+      } else
         e = cudaMemcpy2DAsync(a.d, size_t(dp), a.s, size_t(sp), size_t(a.n), rows, cudaMemcpyDefault, stream);
       if (e != cudaSuccess) return e;
     } else {

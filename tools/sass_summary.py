@@ -11,7 +11,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2506_15155_b200", "libellm.so")
 KEYS = ["UTMALDG", "UTMASTG", "UBLKCP", "UTCHMMA", "UTCQMMA", "UTCBAR", "LDTM", "STTM", "UTCATOMSWS",
-        "HMMA", "SYNCS", "MUFU.EX2", "LDS", "STS", "LDG", "STG", "ATOMG", "RED", "MEMBAR", "FENCE"]
+        "HMMA", "SYNCS", "MUFU.EX2", "LDS", "STS", "LDG", "STG", "ATOMG", "REDG", "MEMBAR", "FENCE"]
 
 
 def demangle(names):
