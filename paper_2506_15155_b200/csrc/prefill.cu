@@ -35,10 +35,12 @@ constexpr int kN = 128;         // keys per tile
 constexpr int kQTiles = 2;      // Q tiles per CTA (ping-pong: one tile's softmax hides the other's MMAs)
 constexpr int kKStages = 2;     // K ring depth
 constexpr int kVStages = 2;     // V ring depth
-constexpr int kSoftmaxWarps = 4 * kQTiles;
-constexpr int kThreads = 64 + 32 * kSoftmaxWarps;  // warp 0 TMA, warp 1 MMA, 4 softmax warps per Q tile
+constexpr int kSplit = 2;       // softmax warps per (Q tile, TMEM lane quarter): each owns kN / kSplit keys
+constexpr int kSoftmaxWarps = 4 * kQTiles * kSplit;
+constexpr int kThreads = 64 + 32 * kSoftmaxWarps;  // warp 0 TMA, warp 1 MMA, 8 softmax warps per Q tile
 constexpr uint32_t kTmemCols = 512;
-constexpr float kRescaleHeadroom = 8.f;  // log2 units: P <= 2^8 before O is rescaled
+constexpr float kRescaleHeadroom = 8.f;
+  // log2 units: P <= 2^8 before O is rescaled
 
 template <int D>
 struct Layout {
@@ -48,7 +50,8 @@ struct Layout {
   static constexpr int off_k = kQTiles * QT;                // K stage s at off_k + s*TILE
   static constexpr int off_v = off_k + kKStages * TILE;     // V stage s at off_v + s*TILE
   static constexpr int off_bar = off_v + kVStages * TILE;
-  static constexpr int bytes = off_bar + 256 + 1024;
+  static constexpr int off_red = off_bar + 256;  // [2 parities][kQTiles][kSplit][128 rows] fp32: row-max exchange
+  static constexpr int bytes = off_red + 2 * kQTiles * kSplit * kM * 4 + 1024;
   static_assert(bytes <= 232448, "shared memory per CTA");
 };
 
@@ -137,16 +140,22 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool b_mn_major)
   return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(b_mn_major) << 16) | (uint32_t(N >> 3) << 17) |
          (uint32_t(M >> 4) << 24);
 }
+// tcgen05.mma / commit are single-thread instructions: the whole MMA warp runs the issue loop
+// with warp-uniform operands (so they live in uniform registers) and elect.sync picks the one
+// thread that issues (a lane-0-only branch made ptxas wrap every MMA in an elect / broadcast /
+// R2UR loop: ~10 dependent instructions per MMA, measured as the MMA warp's critical path).
 __device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-               : "memory");
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+      : "memory");
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -192,8 +201,8 @@ __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.
 // A operand from tensor memory (P: M=128 lanes x K keys, two bf16 per 32-bit column)
 __device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
@@ -251,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int x = 0; x < kQTiles; ++x) {
       mbar_init(s_full + 8 * x, 1);
-      mbar_init(p_full + 8 * x, 4);
+      mbar_init(p_full + 8 * x, 4 * kSplit);
       mbar_init(o_full + 8 * x, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -340,8 +349,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       e_n1 = e_after;
     }
   } else if (warp == 1) {
-    // ================================ MMA issuer ================================
-    if (lane == 0) {
+    // ================================ MMA issuer (whole warp, one elected thread issues) =====
+    {
       constexpr uint32_t id_s = idesc_bf16(kM, kN, false);
       constexpr uint32_t id_pv = idesc_bf16(kM, D, true);
       mbar_wait(q_full, 0);
@@ -386,48 +395,62 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ================================ softmax ================================
-    // warps 2..5 -> Q tile 0, warps 6..9 -> Q tile 1; thread = TMEM lane = MMA row
-    const int x = (warp - 2) >> 2;
+    // warps 2..9 -> Q tile 0, 10..17 -> Q tile 1. Thread = TMEM lane = MMA row; the two warps of a
+    // (Q tile, lane quarter) pair split the tile's 128 keys into halves h = 0 / 1 and exchange
+    // their row maxima through shared memory (named barrier per pair), so twice as many warps
+    // keep the SFU (16 exp2 per SM-cycle: the per-tile budget at full tensor rate) busy.
+    const int sw = warp - 2;
+    const int x = sw / (4 * kSplit);
+    const int h = (sw / 4) % kSplit;
     const int quarter = warp & 3;           // TMEM lanes [32*quarter, 32*quarter + 32) (warp % 4 rule)
     const int row = quarter * 32 + lane;
     const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16);
-    const uint32_t s_col = x * 128, o_col = 256 + x * 128;
+    constexpr int KH = kN / kSplit;         // keys of this warp's half
+    const uint32_t s_col = x * 128 + h * KH, p_col = x * 128 + h * (KH / 2), o_col = 256 + x * 128 + h * (D / kSplit);
     const int g = p.group;
     const int pos_idx = x * bp + row / g;
     const bool valid = pos_idx < n_valid;
     const int prow = valid ? p0 + pos_idx : p0;  // causal limit of this row
+    const uint32_t pair_bar = 1 + x * 4 + quarter;  // named barrier of the two halves' warps
+    float* red = reinterpret_cast<float*>(smem + LY::off_red);
+    auto red_at = [&](int par, int hh) -> float& { return red[((par * kQTiles + x) * kSplit + hh) * kM + row]; };
     if (x < nq) {
       float m_run = -INFINITY, l_run = 0.f;
       for (int t = 0; t < n_tiles; ++t) {
         // S_x(t) complete implies P_x(t-1).V(t-1) complete (commit order): O_x and P_x are free
         mbar_wait(s_full + 8 * x, t & 1);
         tc_fence_after();
-        float xs[kN];
+        float xs[KH];
 #pragma unroll
-        for (int c = 0; c < kN / 32; ++c) tmem_ld32(lane_addr + s_col + c * 32, reinterpret_cast<uint32_t*>(xs + 32 * c));
+        for (int c = 0; c < KH / 32; ++c) tmem_ld32(lane_addr + s_col + c * 32, reinterpret_cast<uint32_t*>(xs + 32 * c));
         tmem_wait_ld();
-        const int lim = prow - t * kN;  // keys j <= lim of this tile are visible
-        if (!__all_sync(0xffffffffu, lim >= kN - 1)) {  // diagonal / last tiles only
+        const int lim = prow - t * kN - h * KH;  // keys j <= lim of this half are visible
+        if (!__all_sync(0xffffffffu, lim >= KH - 1)) {  // diagonal / last tiles only
 #pragma unroll
-          for (int j = 0; j < kN; ++j)
+          for (int j = 0; j < KH; ++j)
             if (j > lim) xs[j] = -INFINITY;
         }
         float mx[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) mx[i] = xs[i];
 #pragma unroll
-        for (int j = 8; j < kN; ++j) mx[j & 7] = fmaxf(mx[j & 7], xs[j]);
-        const float m_tile =
-            fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) *
-            p.scale_log2;
+        for (int j = 8; j < KH; ++j) mx[j & 7] = fmaxf(mx[j & 7], xs[j]);
+        const float m_half =
+            fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        // exchange with the other half (parity-buffered: the partner is at most one tile apart);
+        // the barrier also orders both halves' S loads before either overwrites S with P
+        red_at(t & 1, h) = m_half;
+        asm volatile("bar.sync %0, %1;" ::"r"(pair_bar), "n"(32 * kSplit) : "memory");
+        const float m_tile = fmaxf(m_half, red_at(t & 1, h ^ 1)) * p.scale_log2;
         // lazy rescale: the reference max moves only when the tile max exceeds it by more than
-        // the headroom; the TMEM round trip of O is warp-uniform (tcgen05.ld/st are .aligned)
+        // the headroom (both halves see the same m_tile, so they decide alike); each warp
+        // rescales its half of O_x's columns (tcgen05.ld/st are .aligned: warp-uniform branch)
         const bool grow = m_tile > m_run + kRescaleHeadroom;
         if (t > 0 && __any_sync(0xffffffffu, grow)) {
           const float alpha = grow ? ex2(m_run - m_tile) : 1.f;
           l_run *= alpha;
 #pragma unroll 1
-          for (int c = 0; c < D / 16; ++c) {  // 16 columns at a time: the 128 scores stay live
+          for (int c = 0; c < D / kSplit / 16; ++c) {
             uint32_t o[16];
             tmem_ld16(lane_addr + o_col + c * 16, o);
             tmem_wait_ld();
@@ -440,10 +463,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         float2 sm[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                         make_float2(0.f, 0.f)};
         const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-m_run, -m_run);
-        // exponentials, packed to bf16 pairs and stored over S_x's first 64 columns 32 keys at a
-        // time (P_x: the A operand of P.V, read from TMEM); scaling and sums on fp32 pairs
+        // exponentials, packed to bf16 pairs and stored as P_x's columns [32h, 32h + 32) (keys
+        // 64h .. 64h + 63; the A operand of P.V, read from TMEM); scaling and sums on fp32 pairs
 #pragma unroll
-        for (int c = 0; c < kN / 32; ++c) {
+        for (int c = 0; c < KH / 32; ++c) {
           uint32_t pk[16];
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
@@ -453,17 +476,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             sm[(j >> 1) & 3] = fadd2(sm[(j >> 1) & 3], make_float2(a, b));
             pk[j / 2] = pack_bf16(a, b);
           }
-          tmem_st16(lane_addr + s_col + c * 16, pk);
+          tmem_st16(lane_addr + p_col + c * 16, pk);
         }
         l_run += ((sm[0].x + sm[0].y) + (sm[1].x + sm[1].y)) + ((sm[2].x + sm[2].y) + (sm[3].x + sm[3].y));
-        if (x == 0 && t == n_tiles - 1) {  // V rows past the last visible key may hold anything
+        if (x == 0 && h == 0 && t == n_tiles - 1) {  // V rows past the last visible key may hold anything
           const int need = last_key + 1 - t * kN;
           if (row >= need) {
             uint8_t* vrow = smem + LY::off_v + (t % kVStages) * LY::TILE + row * 128;
 #pragma unroll
-            for (int h = 0; h < HALVES; ++h)
+            for (int hf = 0; hf < HALVES; ++hf)
 #pragma unroll
-              for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(vrow + h * kN * 128 + c * 16) = make_uint4(0, 0, 0, 0);
+              for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(vrow + hf * kN * 128 + c * 16) = make_uint4(0, 0, 0, 0);
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
@@ -472,13 +495,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full + 8 * x);
       }
-      // ---- epilogue: O_x / l -> bf16 -> out[q_row0 + pos][kvh*group + head][:] ----
+      // ---- epilogue: O_x / (l_h0 + l_h1) -> bf16 -> out[q_row0 + pos][kvh*group + head][h half] ----
+      red_at(n_tiles & 1, h) = l_run;
+      asm volatile("bar.sync %0, %1;" ::"r"(pair_bar), "n"(32 * kSplit) : "memory");
+      const float inv = 1.f / (l_run + red_at(n_tiles & 1, h ^ 1));
       mbar_wait(o_full + 8 * x, 0);
       tc_fence_after();
-      const float inv = 1.f / l_run;
-      __nv_bfloat16* dst = p.out + (int64_t(q_row0 + pos_idx) * p.Hq + kvh * g + row % g) * D;
+      __nv_bfloat16* dst = p.out + (int64_t(q_row0 + pos_idx) * p.Hq + kvh * g + row % g) * D + h * (D / kSplit);
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < D / kSplit / 32; ++c) {
         uint32_t o[32];
         tmem_ld32(lane_addr + o_col + c * 32, o);
         tmem_wait_ld();
@@ -520,13 +545,13 @@ cudaError_t launch_de(const PrefillMaps& maps, const PParams& prm, int n_work, c
 constexpr int kDefaultEmu = 0;  // measured: MUFU for all (1187 vs 1094 TFLOP/s at 2 x 4K over 32K)
 template <int D>
 cudaError_t launch_d(const PrefillMaps& maps, const PParams& prm, int n_work, cudaStream_t s) {
-  const char* v = std::getenv("ELLM_PF_EMU");  // measurement knob: 0, 2, 3 or 4 of every 8
+  const char* v = std::getenv("ELLM_PF_EMU");  // measurement knob: 0, 1, 2 or 3 of every 8
   const int emu = v ? std::atoi(v) : kDefaultEmu;
   switch (emu) {
-    case 0: return launch_de<D, 0>(maps, prm, n_work, s);
+    case 1: return launch_de<D, 1>(maps, prm, n_work, s);
+    case 2: return launch_de<D, 2>(maps, prm, n_work, s);
     case 3: return launch_de<D, 3>(maps, prm, n_work, s);
-    case 4: return launch_de<D, 4>(maps, prm, n_work, s);
-    default: return launch_de<D, 2>(maps, prm, n_work, s);
+    default: return launch_de<D, 0>(maps, prm, n_work, s);
   }
 }
 
