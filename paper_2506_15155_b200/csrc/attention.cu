@@ -32,14 +32,6 @@
 namespace ellm {
 namespace {
 
-#ifndef ELLM_MERGE_DEPTH
-#define ELLM_MERGE_DEPTH 8   // record loads in flight per lane in the end-of-CTA merges
-#endif
-#ifndef ELLM_MERGE_ROW_UNROLL
-#define ELLM_MERGE_ROW_UNROLL 1
-#endif
-#define ELLM_PRAGMA_S(x) _Pragma(#x)
-#define ELLM_PRAGMA(x) ELLM_PRAGMA_S(x)
 constexpr int kConsumerWarps = 8;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 
@@ -188,100 +180,124 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 constexpr int kFirst = 1, kLast = 2, kDone = 4;  // stage metadata flags
 
-// LSE merge of the partial records of virtual request vr, run by the 256
-// consumer threads of the last CTA to finish it:
+// LSE merge of the partial records of virtual request vr, run by warps
+// [w0, w0 + nw) of the last CTA to finish it:
 //   M = max_p m_p,  L = sum_p 2^(m_p - M) l_p,  o = sum_p 2^(m_p - M) o_p / L   -> bf16 (RNE).
-// LPR = D/4 lanes own one q-head row (a float4 of o each): the max and the sum over records
-// are lane-parallel reductions, each record's weight is broadcast by shuffle, and a record's o
-// row is one coalesced D*4-byte load across the row's lanes. Records written by other SMs are
-// read through L2 (__ldcg): L1 is not coherent across SMs.
-template <int D, int DEPTH>  // DEPTH: record loads in flight per lane (register cost 5*DEPTH)
-__device__ __forceinline__ void merge_request(const Params& p, int vr, int rows, int nsub, int HB, int w0,
-                                              int nw) {  // run by warps [w0, w0 + nw)
-  constexpr int LPR = D / 4;         // lanes per row
-  constexpr int RPW = 32 / LPR;      // rows per warp pass
+// TPR = D / (4 VEC) lanes own one q-head row, VEC float4 of o each (VEC grows with the row count
+// so that more rows of the request are in flight at once: 8 rows -> VEC 1 ... 32+ rows -> VEC 4;
+// measured at C4, 64 rows: 12.6 us with one row per warp pass). In one pass over the records (in
+// chunks of TPR): lane k of a row loads record k's (m, l); the chunk max, the weights (broadcast by
+// shuffle) and the o rows follow, DEPTH records' VEC float4 loads in flight per lane; a later chunk
+// with a larger max rescales what is accumulated. Records written by other SMs are read through L2
+// (__ldcg): L1 is not coherent across SMs.
+template <int D, int VEC, int DEPTH>  // DEPTH: records per load batch (DEPTH x VEC float4 per lane)
+__device__ __forceinline__ void merge_rows(const Params& p, int vr, int rows, int HB, int w0, int nw) {
+  constexpr int TPR = D / 4 / VEC;   // lanes per row
+  constexpr int RPW = 32 / TPR;      // rows per warp pass
   // record ranges: static owners (CTAs b), then dynamic owners (units u); record id of
-  // (owner, vr) is owner + vr, each with nsub subtile slots
-  const int64_t s0 = int64_t(__ldg(p.b_first + vr) + vr) * nsub;
-  const int64_t ns = int64_t(__ldg(p.b_last + vr) - __ldg(p.b_first + vr) + 1) * nsub;
-  const int64_t d0 = int64_t(p.rec_dyn + __ldg(p.u_first + vr) + vr) * nsub;
-  const int64_t nd = int64_t(__ldg(p.u_last + vr) - __ldg(p.u_first + vr) + 1) * nsub;  // 0 if none
+  // (owner, vr) is owner + vr (one record per q-head row: subtile partials are combined in-CTA)
+  const int64_t s0 = int64_t(__ldg(p.b_first + vr) + vr);
+  const int64_t ns = int64_t(__ldg(p.b_last + vr) - __ldg(p.b_first + vr) + 1);
+  const int64_t d0 = int64_t(p.rec_dyn + __ldg(p.u_first + vr) + vr);
+  const int64_t nd = int64_t(__ldg(p.u_last + vr) - __ldg(p.u_first + vr) + 1);  // 0 if none
   const int64_t P = ns + nd;
   auto pid = [&](int64_t k) { return k < ns ? s0 + k : d0 + (k - ns); };
   const int ireq = vr / p.HG, hg = vr % p.HG;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int e4 = lane % LPR, sub = lane / LPR;
-  const unsigned seg_mask = RPW == 1 ? 0xffffffffu : (0xffffu << (16 * sub));
-  ELLM_PRAGMA(unroll ELLM_MERGE_ROW_UNROLL)
+  const int e4 = lane % TPR, sub = lane / TPR;
+  const unsigned seg_mask = RPW == 1 ? 0xffffffffu : (((1u << TPR) - 1u) << (TPR * sub));
   for (int row0 = (warp - w0) * RPW; row0 < rows; row0 += nw * RPW) {
     const int row = row0 + sub;
     const bool live = row < rows;
-    // one pass over the records in chunks of LPR (usually one chunk): lane e4 loads record
-    // base+e4's (m, l) — the chunk's max and weights need no second load — then the o rows in
-    // batches of DEPTH independent loads; a later chunk with a larger max rescales what is
-    // accumulated (same LSE rule). Round trips to L2: 1 + ceil(P / DEPTH) instead of
-    // 2 + ceil(P / DEPTH) plus a separate max pass.
     float M = -INFINITY, L = 0.f;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int64_t base = 0; base < P; base += LPR) {
+    float4 acc[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t base = 0; base < P; base += TPR) {
       const int64_t mk = base + e4;
       float2 ml = make_float2(-INFINITY, 0.f);
       if (live && mk < P) ml = __ldcg(reinterpret_cast<const float2*>(p.part_ml + (pid(mk) * rows + row) * 2));
       float cm = ml.x;
 #pragma unroll
-      for (int o = LPR / 2; o > 0; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(seg_mask, cm, o));
+      for (int o = TPR / 2; o > 0; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(seg_mask, cm, o));
       const float Mn = fmaxf(M, cm);
       if (Mn > M && M != -INFINITY) {  // a later chunk raised the max: rescale (segment-uniform)
         const float sc = ex2(M - Mn);
         L *= sc;
-        acc.x *= sc;
-        acc.y *= sc;
-        acc.z *= sc;
-        acc.w *= sc;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          acc[v].x *= sc;
+          acc[v].y *= sc;
+          acc[v].z *= sc;
+          acc[v].w *= sc;
+        }
       }
       M = Mn;
       // a record with no valid token has m = -inf -> weight 0 (and so does every lane past P)
       const float my_w = (M == -INFINITY || ml.x == -INFINITY) ? 0.f : ex2(ml.x - M);
       L += my_w * ml.y;
-      const int cnt = int(min(int64_t(LPR), P - base));
-      for (int j0 = 0; j0 < cnt; j0 += DEPTH) {  // DEPTH independent record loads in flight
-        float4 ov[DEPTH];
+      const int cnt = int(min(int64_t(TPR), P - base));
+      for (int j0 = 0; j0 < cnt; j0 += DEPTH) {
+        float4 ov[DEPTH][VEC];
         float wv[DEPTH];
 #pragma unroll
         for (int jj = 0; jj < DEPTH; ++jj) {
           const int j = j0 + jj;
-          wv[jj] = __shfl_sync(seg_mask, my_w, j & (LPR - 1), LPR);  // 0 for lanes past P
-          ov[jj] = (live && j < cnt)
-                       ? __ldcg(reinterpret_cast<const float4*>(p.part + (pid(base + j) * rows + row) * D) + e4)
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
+          wv[jj] = __shfl_sync(seg_mask, my_w, j % TPR, TPR);  // 0 for lanes past P
+          const float4* rec = reinterpret_cast<const float4*>(p.part + (pid(base + j) * rows + row) * D);
+#pragma unroll
+          for (int v = 0; v < VEC; ++v)
+            ov[jj][v] = (live && j < cnt) ? __ldcg(rec + e4 + TPR * v) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int jj = 0; jj < DEPTH; ++jj) {
           const float w = (j0 + jj < cnt) ? wv[jj] : 0.f;
-          acc.x += w * ov[jj].x;
-          acc.y += w * ov[jj].y;
-          acc.z += w * ov[jj].z;
-          acc.w += w * ov[jj].w;
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            acc[v].x += w * ov[jj][v].x;
+            acc[v].y += w * ov[jj][v].y;
+            acc[v].z += w * ov[jj][v].z;
+            acc[v].w += w * ov[jj][v].w;
+          }
         }
       }
     }
 #pragma unroll
-    for (int o = LPR / 2; o > 0; o >>= 1) L += __shfl_xor_sync(seg_mask, L, o);
+    for (int o = TPR / 2; o > 0; o >>= 1) L += __shfl_xor_sync(seg_mask, L, o);
     if (live) {
       const float inv = 1.f / L;
-      __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
-      __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
-      uint2 v;
-      v.x = *reinterpret_cast<uint32_t*>(&lo);
-      v.y = *reinterpret_cast<uint32_t*>(&hi);
-      if (p.n_peer == 0) {
-        *reinterpret_cast<uint2*>(p.out + (int64_t(ireq) * p.Hq + hg * HB * p.group + row) * D + 4 * e4) = v;
-      } else {  // a10: the row goes to every rank's window (own window included)
-        const int64_t off = (int64_t(ireq) * p.Hq_out + p.q_off + hg * HB * p.group + row) * D + 4 * e4;
-        for (int i = 0; i < p.n_peer; ++i) *reinterpret_cast<uint2*>(p.gout[i] + off) = v;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(acc[v].x * inv, acc[v].y * inv);
+        __nv_bfloat162 hi = __floats2bfloat162_rn(acc[v].z * inv, acc[v].w * inv);
+        uint2 u;
+        u.x = *reinterpret_cast<uint32_t*>(&lo);
+        u.y = *reinterpret_cast<uint32_t*>(&hi);
+        const int col = 4 * (e4 + TPR * v);
+        if (p.n_peer == 0) {
+          *reinterpret_cast<uint2*>(p.out + (int64_t(ireq) * p.Hq + hg * HB * p.group + row) * D + col) = u;
+        } else {  // a10: the row goes to every rank's window (own window included)
+          const int64_t off = (int64_t(ireq) * p.Hq_out + p.q_off + hg * HB * p.group + row) * D + col;
+          for (int i = 0; i < p.n_peer; ++i) *reinterpret_cast<uint2*>(p.gout[i] + off) = u;
+        }
       }
     }
   }
+}
+// End-of-CTA merges: one instantiation per kernel (a runtime choice among several inlined variants
+// raised the streaming loop's register pressure into spills), VEC sized for the largest row count
+// the head block can have (rows = HB * group <= 8 HB): HB = 1 -> VEC 1, HB = 2 -> 2, HB >= 4 -> 4
+// (C2: 32 rows in one pass of 256 lanes; the 70B shape's 64 rows in two). The merge warp 0 runs
+// mid-stream when its deferred list is full is the lean DEPTH-1 form (it sits inside the
+// streaming loop: a wider one there pushed the loop into spills, 25% slower launches at C2).
+template <int D, int HB>
+__device__ __forceinline__ void merge_request(const Params& p, int vr, int rows, int w0, int nw) {
+  constexpr int VEC = D == 64 ? (HB >= 2 ? 2 : 1) : (HB >= 4 ? 4 : HB);
+  merge_rows<D, VEC, 8 / VEC>(p, vr, rows, HB, w0, nw);
+}
+template <int D>
+__device__ __forceinline__ void merge_request_lean(const Params& p, int vr, int rows, int HB) {
+  merge_rows<D, 1, 1>(p, vr, rows, HB, 0, 1);
 }
 
 // One thread spins (acquire, system scope) until *flag - target >= 0 (wrapping counters);
@@ -806,7 +822,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (__shfl_sync(0xffffffffu, now, 0)) {
-        merge_request<D, 1>(p, vr, rows, 1, HB, 0, 1);
+        merge_request_lean<D>(p, vr, rows, HB);
         if (lane == 0) ++s_n_now;
       }
     }
@@ -816,7 +832,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
   __threadfence();
   for (int k = 0; k < s_n_merge; ++k)
-    merge_request<D, ELLM_MERGE_DEPTH>(p, s_merge[k], rows, 1, HB, 0, kConsumerWarps);
+    merge_request<D, HB>(p, s_merge[k], rows, 0, kConsumerWarps);
   if (p.trace && threadIdx.x == 0) {
     p.trace[blockIdx.x * 8 + 4] = gtimer();
     p.trace[blockIdx.x * 8 + 6] = (unsigned long long)(s_n_merge + s_n_now);
