@@ -401,6 +401,9 @@ int64_t ellm_kernel_launches(const ellm_pool* pool);
  * [4] merges done, [5] end, all %globaltimer ns (0 = not reached), [6] requests merged, [7] SM id.
  * NULL disables. launches < 0 or (buffer with launches == 0) -> INVALID_ARG. */
 int ellm_set_attn_trace(ellm_pool* pool, void* device_buf, int32_t launches);
+/* Measurement knob: split the attention kernel's static work over CTA b in proportion to w[b]
+ * (n >= the launch's CTA count; n = 0 restores equal shares). Outputs stay within R8. */
+int ellm_debug_attn_weights(ellm_pool* pool, const float* w, int32_t n);
 
 #ifdef __cplusplus
 }

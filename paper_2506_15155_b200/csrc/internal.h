@@ -283,6 +283,7 @@ struct ellm_pool {
   uint32_t gdone_base = 0;                 // gather-launch CTAs counted by earlier launches
   unsigned long long* trace_buf = nullptr; // ellm_set_attn_trace: caller's device buffer
   int32_t trace_slots = 0;
+  std::vector<float> dbg_weights;          // ellm_debug_attn_weights: static split weights per CTA
   int64_t trace_launch = 0;
   int64_t dyn_div = 0;                     // dynamic tail = tiles/dyn_div per request (0: static only)
   int64_t dyn_unit = 8;                    // minimum tiles per dynamic unit

@@ -412,6 +412,13 @@ const char* ellm_status_string(int s) {
 int ellm_last_cuda_error(const ellm_pool* p) { return p ? p->last_cuda_error : 0; }
 int64_t ellm_kernel_launches(const ellm_pool* p) { return p ? p->launches : 0; }
 
+int ellm_debug_attn_weights(ellm_pool* p, const float* w, int32_t n) {
+  if (!p || n < 0 || (n > 0 && !w)) return ELLM_ERR_INVALID_ARG;
+  p->dbg_weights.assign(w, w + n);
+  p->cache_key.clear();
+  return ELLM_OK;
+}
+
 int ellm_set_attn_trace(ellm_pool* p, void* device_buf, int32_t launches) {
   if (!p || launches < 0 || (device_buf && launches == 0)) return ELLM_ERR_INVALID_ARG;
   if (!p->has_dev) return ELLM_ERR_NO_DEVICE;
@@ -991,7 +998,21 @@ static int attention_impl(ellm_pool* p, int32_t layer, int32_t n, const int32_t*
     // owns [u U, (u+1) U).
     const int64_t G = pl.G;
     std::vector<int64_t> B(size_t(G) + 1);
-    for (int64_t b = 0; b <= G; ++b) B[size_t(b)] = b * Ws / G;
+    if (int64_t(p->dbg_weights.size()) >= G) {  // measurement knob (ellm_debug_attn_weights)
+      double tot = 0.0;
+      for (int64_t b = 0; b < G; ++b) tot += p->dbg_weights[size_t(b)];
+      double acc = 0.0;
+      B[0] = 0;
+      for (int64_t b = 1; b < G; ++b) {
+        acc += p->dbg_weights[size_t(b - 1)];
+        int64_t t = int64_t(double(Ws) * acc / tot + 0.5);
+        t = std::min(std::max(t, B[size_t(b - 1)] + 1), Ws - (G - b));
+        B[size_t(b)] = t;
+      }
+      B[size_t(G)] = Ws;
+    } else {
+      for (int64_t b = 0; b <= G; ++b) B[size_t(b)] = b * Ws / G;
+    }
     auto cta_of = [&](int64_t t) {  // the CTA holding static tile t
       return int32_t(std::upper_bound(B.begin(), B.end(), t) - B.begin()) - 1;
     };

@@ -103,6 +103,7 @@ _SIGS = {
     "ellm_gather_wait": (ctypes.c_int, [_P, _I32, _V]),
     "ellm_gather_wait_next": (ctypes.c_int, [_P, _I32]),
     "ellm_set_attn_trace": (ctypes.c_int, [_P, _V, _I32]),
+    "ellm_debug_attn_weights": (ctypes.c_int, [_P, _P, _I32]),
     "ellm_memcpy_async": (ctypes.c_int, [_V, _V, _I64, _V]),
     "ellm_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "ellm_last_cuda_error": (ctypes.c_int, [_P]),
@@ -225,6 +226,11 @@ class Pool:
 
     def gather_wait(self, layer, stream=None) -> int:
         return ellm_gather_wait(self._h, int(layer), _sptr(stream))
+
+    def debug_attn_weights(self, w) -> int:
+        """Static split weights per attention CTA (measurement knob); [] restores equal shares."""
+        a = np.ascontiguousarray(np.asarray(w, dtype=np.float32))
+        return ellm_debug_attn_weights(self._h, a.ctypes.data_as(ctypes.c_void_p) if a.size else None, int(a.size))
 
     def set_attn_trace(self, device_buf, launches: int) -> int:
         """Per-CTA timeline stamps of the next attention launches (profiling)."""
