@@ -303,3 +303,14 @@ def test_attention_is_deterministic(dyn, monkeypatch):
         assert t.p.attention(0, [2, 0, 3, 1], q, out, t.scale) == 0
         torch.cuda.synchronize()
         assert np.array_equal(torch_to_bits(out), first)
+
+
+def test_attention_list_longer_than_max_requests():
+    """a request list with repeated ids may be longer than max_requests; the split-K
+    state grows (device-synchronising) instead of being overrun, and every entry is correct."""
+    t = Twin(1, 32, 8, 128, 16, 300, 300, 2, 150, 0, seed=19)
+    assert t.reserve([0, 1], [1500, 333]) == 0
+    t.append_all_layers([0, 1], [1500, 333])
+    t.attention(0, [0, 1] * 5)           # 10 entries, max_requests 2
+    t.attention(0, [1, 1, 1, 0] * 8)     # 32 entries: grows again
+    t.attention(0, [1, 0])               # and the small list still works afterwards

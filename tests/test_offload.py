@@ -37,6 +37,31 @@ def test_offload_metadata_matches_oracle_deflate():
     assert p.release(0) == 0 and p.stats()["host_used"] == len(ids)
 
 
+def test_offload_commit_needs_every_layer_not_a_count():
+    """offload_commit checks which layers were copied (a per-chunk bitset), not how many calls
+    were made: copying layer 0 L times does not make layers 1..L-1 copied."""
+    L = 3
+    p = ellm.Pool(ellm.DEVICE_NONE, L, 4, 2, 64, 16, 40, 40, 3, 12, 24)
+    assert p.reserve([0], [70]) == 0
+    ids = p.table(0)[0].tolist()
+    assert p.offload_begin(ids)[0] == 0
+    for _ in range(L):
+        assert p.offload_layer(0, ids) == 0
+    assert p.offload_commit(ids) == ellm.INVALID_ARG
+    assert p.offload_layer(2, ids) == 0
+    assert p.offload_commit(ids) == ellm.INVALID_ARG      # layer 1 still missing
+    assert p.offload_layer(1, ids[1:]) == 0               # ... for one chunk
+    assert p.offload_commit(ids) == ellm.INVALID_ARG
+    assert p.offload_layer(1, ids[:1]) == 0
+    assert p.offload_commit(ids) == 0
+    # a fresh offload of other chunks starts with no layer marked
+    assert p.reserve([1], [40]) == 0
+    ids1 = p.table(1)[0].tolist()
+    assert p.offload_begin(ids1)[0] == 0
+    assert p.offload_layer(0, ids1) == 0 and p.offload_layer(1, ids1) == 0
+    assert p.offload_commit(ids1) == ellm.INVALID_ARG
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode,rotate", [(0, "0"), (1, "0"), (0, "1"), (1, "1")])
 def test_offload_layerwise_bytes_overlapped_with_appends(mode, rotate, monkeypatch):

@@ -16,9 +16,10 @@ from inputs import workload as W  # noqa: E402
 def main():
     wname = sys.argv[1] if len(sys.argv) > 1 else "c4"
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+    pdl = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     wl = W.c4(n, 0) if wname == "c4" else W.c2(n, 0)
     pool = W.make_pool(wl, 0)
-    pool.set_launch_overlap(False)
+    pool.set_launch_overlap(bool(pdl))
     W.prefill(pool, wl)
     L, B = wl.n_layers, wl.batch
     reqs, ones = list(range(B)), [1] * B
@@ -47,6 +48,7 @@ def main():
 
     def summary(t, label):
         spans, ends, durs = [], [], []
+        per = [(t[i + 1][:, 0].min() - t[i][:, 0].min()) / 1e3 for i in range(t.shape[0] - 1)]
         for i in range(t.shape[0]):
             x = t[i]
             t0 = x[:, 0].min()
@@ -56,12 +58,12 @@ def main():
             durs.append(x[:, 3] - x[:, 2])
         e = np.median(np.array(ends), axis=0)
         d = np.median(np.array(durs), axis=0)
-        print(f"{label:28s} span {np.median(spans):8.2f} us; streaming end min/med/max {e[0]:.2f} / {e[1]:.2f} / "
+        print(f"{label:28s} period {np.median(per):8.2f} span {np.median(spans):8.2f} us; streaming end min/med/max {e[0]:.2f} / {e[1]:.2f} / "
               f"{e[2]:.2f} us; per-CTA duration / median: {d.min() / np.median(d):.3f} .. {d.max() / np.median(d):.3f}")
         return d
 
     run(2, False)
-    d0 = summary(run(2, True), f"{wl.name} x{n} equal shares")
+    d0 = summary(run(2, True), f"{wl.name} x{n} pdl {pdl} equal shares")
     w = np.full(G, 1.0)
     share = np.full(G, 1.0)
     d = d0
