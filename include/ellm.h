@@ -399,7 +399,9 @@ int64_t ellm_kernel_launches(const ellm_pool* pool);
  * (counted from this call) writes, per CTA b, into slot (k % launches): [b*8 + 0] start,
  * [1] producer past griddepcontrol.wait, [2] first stage data seen, [3] streaming done,
  * [4] merges done, [5] end, all %globaltimer ns (0 = not reached), [6] requests merged, [7] SM id.
- * NULL disables. launches < 0 or (buffer with launches == 0) -> INVALID_ARG. */
+ * NULL disables. launches < 0 or (buffer with launches == 0) -> INVALID_ARG. While set, every
+ * prefill launch also writes, for its first CTA and key tiles t < 16, clock64 stamps of the
+ * TMA / MMA / softmax hand-offs into words [t*16 + 0..13] of the buffer (tools/pf_timeline.py). */
 int ellm_set_attn_trace(ellm_pool* pool, void* device_buf, int32_t launches);
 /* Measurement knob: split the attention kernel's static work over CTA b in proportion to w[b]
  * (n >= the launch's CTA count; n = 0 restores equal shares). Outputs stay within R8. */

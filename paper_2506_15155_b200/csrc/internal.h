@@ -210,7 +210,7 @@ cudaError_t encode_prefill_kv_maps(PrefillMaps* m, void* pool_base, int64_t max_
 cudaError_t encode_prefill_q_map(PrefillMaps* m, const AttnShape& sh, const void* q, int64_t q_rows);
 cudaError_t launch_prefill_attention(const PrefillMaps& maps, const AttnShape& sh, const int32_t* work,
                                      int32_t n_work, const int32_t* table, int32_t table_stride, int32_t layer,
-                                     void* out, float scale, cudaStream_t s);
+                                     void* out, float scale, cudaStream_t s, void* trace = nullptr);
 
 }  // namespace ellm
 

@@ -1710,7 +1710,7 @@ int ellm_prefill_attention(ellm_pool* p, int32_t layer, int32_t n, const int32_t
     for (int64_t b = 0; b < n_q[i]; b += bp) {
       const int64_t pos0 = len - n_q[i] + b;
       const int64_t nv = std::min<int64_t>(bp, n_q[i] - b);
-      const int64_t tiles = (pos0 + nv + 127) / 128;  // keys 0 .. pos0 + nv - 1
+      const int64_t tiles = (pos0 + nv + 127) / 128;  // 128-key tiles (prefill.cu kN) over keys 0 .. pos0 + nv - 1
       for (int32_t h = 0; h < p->cfg.n_heads_kv; ++h)
         items.push_back({{r, int32_t(len), int32_t(row0 + b), int32_t(pos0), int32_t(nv), h, int32_t(tiles), 0}});
     }
@@ -1731,7 +1731,7 @@ int ellm_prefill_attention(ellm_pool* p, int32_t layer, int32_t n, const int32_t
   }
   if ((e = encode_prefill_q_map(&p->pf_maps, p->ash, q, rows)) != cudaSuccess) return cuda_fail(p, e);
   e = launch_prefill_attention(p->pf_maps, p->ash, d_work, int32_t(items.size()), p->d_table,
-                               p->cfg.max_chunks_per_request, layer, out, scale, st);
+                               p->cfg.max_chunks_per_request, layer, out, scale, st, p->trace_buf);
   if (e != cudaSuccess) return cuda_fail(p, e);
   ++p->launches;
   return p->ring.commit(st);
