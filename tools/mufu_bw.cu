@@ -27,6 +27,20 @@ __global__ void k(int iters, float* out, unsigned long long* cyc) {
         asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(r) : "r"(__float_as_uint(v[i])));
         v[i] = __uint_as_float(r);
       }
+      if (OP == 4) {  // F2FP: two fp32 -> packed bf16x2 (round to nearest even)
+        uint32_t r;
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(v[i]), "f"(v[(i + 1) & 31]));
+        v[i] = __uint_as_float(r ^ 0x3f803f80u);
+      }
+      if (OP == 5) {  // MUFU.EX2 and F2FP interleaved 1:1
+        uint32_t r;
+        if (i & 1) {
+          asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(v[i]), "f"(v[i - 1]));
+          v[i] = __uint_as_float(r ^ 0x3f803f80u);
+        } else {
+          asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(v[i]));
+        }
+      }
     }
   }
   __syncthreads();
@@ -42,15 +56,17 @@ int main() {
   unsigned long long* cyc;
   cudaMalloc(&out, 4 * 148 * 1024);
   cudaMalloc(&cyc, 8 * 148);
-  const char* names[] = {"MUFU.EX2 f32", "FFMA", "FFMA2 (f32x2)", "MUFU.EX2 bf16x2"};
+  const char* names[] = {"MUFU.EX2 f32", "FFMA", "FFMA2 (f32x2)", "MUFU.EX2 bf16x2", "F2FP bf16x2", "EX2+F2FP 1:1"};
   const int iters = 4096;
-  for (int op = 0; op < 4; ++op)
+  for (int op = 0; op < 6; ++op)
     for (int warps : {4, 8, 16}) {
       switch (op) {
         case 0: k<0><<<148, warps * 32>>>(iters, out, cyc); break;
         case 1: k<1><<<148, warps * 32>>>(iters, out, cyc); break;
         case 2: k<2><<<148, warps * 32>>>(iters, out, cyc); break;
         case 3: k<3><<<148, warps * 32>>>(iters, out, cyc); break;
+        case 4: k<4><<<148, warps * 32>>>(iters, out, cyc); break;
+        case 5: k<5><<<148, warps * 32>>>(iters, out, cyc); break;
       }
       unsigned long long h[148];
       cudaMemcpy(h, cyc, 8 * 148, cudaMemcpyDeviceToHost);

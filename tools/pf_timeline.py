@@ -42,7 +42,11 @@ def main():
     print(f"  S1(t+1) issued -> softmax Q1 sees S    {med([t[i + 1, 2] - t[i, 7] for i in rng]):8.0f}")
     print(f"  period (softmax Q0 S-ready to S-ready) {med([t[i + 1, 0] - t[i, 0] for i in rng]):8.0f}")
     print(f"  Q1 S-ready minus Q0 S-ready (phase)    {med([t[i, 2] - t[i, 0] for i in rng]):8.0f}")
-    if not t[:, 8:].any():  # the MMA-loop / producer stamps exist only in some kernel versions
+    if t[:, 8].any() and not t[:, 11].any():  # softmax-phase stamps (Q0, first warp)
+        print(f"  softmax Q0: S ready -> S in registers  {med([t[i, 8] - t[i, 0] for i in rng]):8.0f}")
+        print(f"  softmax Q0: -> pair max exchanged      {med([t[i, 9] - t[i, 8] for i in rng]):8.0f}")
+        print(f"  softmax Q0: -> P stored (exps, st)     {med([t[i, 10] - t[i, 9] for i in rng]):8.0f}")
+    if not t[:, 11:].any():  # the MMA-loop / producer stamps exist only in some kernel versions
         p.close()
         return
     print(f"  MMA loop: top -> V(t) ready            {med([t[i, 9] - t[i, 8] for i in rng]):8.0f}")
