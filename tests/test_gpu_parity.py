@@ -314,3 +314,63 @@ def test_attention_list_longer_than_max_requests():
     t.attention(0, [0, 1] * 5)           # 10 entries, max_requests 2
     t.attention(0, [1, 1, 1, 0] * 8)     # 32 entries: grows again
     t.attention(0, [1, 0])               # and the small list still works afterwards
+
+
+@pytest.mark.parametrize("rotate", ["0", "1"])
+def test_copy_engine_runs_match_oracle(rotate, monkeypatch):
+    """The copy-engine swap path (pool.cpp issue_copies) merges a chunk list into one
+    cudaMemcpyAsync per contiguous run and one cudaMemcpy2DAsync per evenly strided run. Lists
+    mixing a consecutive run, a reversed run, strided ids and singletons — deflated into slots
+    that are consecutive, then inflated from slots in a shuffled order (strided / scattered
+    destinations) — must leave tables and bytes bit-exact with the oracle, canonical and with
+    rotated slabs (per-chunk pieces listed piece-major)."""
+    monkeypatch.setenv("ELLM_ROTATE", rotate)
+    rng = np.random.default_rng(23)
+    t = Twin(3, 8, 2, 128, 16, 160, 160, 4, 60, 160, seed=29)   # 48 KiB chunks, 16 KiB slabs
+    t.p.set_swap_mode(1)
+    lens = [900, 300, 700, 555]
+    assert t.reserve(list(range(4)), lens) == 0
+    t.append_all_layers(list(range(4)), lens)
+    ids0 = t.o.table(0)[0].tolist()          # consecutive ids
+    ids2 = t.o.table(2)[0].tolist()
+    mixed = ids0[:10] + ids2[::-1][:8] + ids0[10:30:3] + [ids2[0]]
+    rc, slots = t.deflate(mixed)
+    assert rc == 0
+    t.check_tables()
+    t.check_bytes()
+    order = rng.permutation(len(slots))
+    rc, _ = t.inflate([int(slots[i]) for i in order[: len(order) // 2]])
+    assert rc == 0
+    rc, _ = t.inflate([int(slots[i]) for i in order[len(order) // 2:]][::-1])
+    assert rc == 0
+    t.check_tables()
+    t.check_bytes()
+    for l in range(3):
+        t.attention(l, [0, 1, 2, 3])
+
+
+def test_trace_and_split_weights_keep_results():
+    """The timeline instrumentation (ellm_set_attn_trace) does not change a launch's bits; the
+    split-weight knob (ellm_debug_attn_weights) changes the partition but stays within R8."""
+    import torch
+    t = Twin(1, 32, 8, 128, 16, 1100, 1100, 4, 400, 0, seed=31)
+    lens = [6000, 300, 2900, 1234]
+    assert t.reserve([0, 1, 2, 3], lens) == 0
+    t.append_all_layers([0, 1, 2, 3], lens)
+    rc, (plain, _) = t.attention(0, [0, 1, 2, 3])
+    assert rc == 0
+    G = torch.cuda.get_device_properties(0).multi_processor_count
+    buf = torch.zeros((2, G, 8), dtype=torch.int64, device="cuda")
+    assert t.p.set_attn_trace(buf, 2) == 0
+    rc, (traced, _) = t.attention(0, [0, 1, 2, 3])
+    assert rc == 0 and np.array_equal(traced, plain)
+    stamps = buf[0].cpu().numpy()
+    live = stamps[:, 0] > 0
+    assert live.sum() > 0 and np.all(stamps[live, 5] >= stamps[live, 0])
+    assert t.p.set_attn_trace(None, 0) == 0
+    w = np.random.default_rng(3).uniform(0.5, 2.0, G)
+    assert t.p.debug_attn_weights(w) == 0
+    t.attention(0, [0, 1, 2, 3])             # checked against the oracle inside
+    assert t.p.debug_attn_weights([]) == 0
+    rc, (again, _) = t.attention(0, [0, 1, 2, 3])
+    assert rc == 0 and np.array_equal(again, plain)
