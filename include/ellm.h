@@ -357,7 +357,9 @@ int ellm_gather_wait(ellm_pool* pool, int32_t layer, void* stream);
  * attention launches, so they still overlap (launch overlap / PDL). Without a following attention
  * launch nothing waits: call gather_wait instead. Requires that the peers' launches progress
  * independently of this launch (one GPU per rank, or ranks sharing one stream): a spinning CTA
- * holds its SM. Errors as gather_wait; no stream argument. */
+ * holds its SM. One wait is pending at a time: a second call before the next attention launch
+ * replaces the first (fold the wait the next launch actually needs). Errors as gather_wait; no
+ * stream argument. */
 int ellm_gather_wait_next(ellm_pool* pool, int32_t layer);
 /* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream): host <-> window copies. */
 int ellm_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
