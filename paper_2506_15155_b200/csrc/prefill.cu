@@ -35,7 +35,10 @@ constexpr int kN = 128;         // keys per tile
 constexpr int kQTiles = 2;      // Q tiles per CTA (ping-pong: one tile's softmax hides the other's MMAs)
 constexpr int kKStages = 2;     // K ring depth
 constexpr int kVStages = 2;     // V ring depth
-constexpr int kSplit = 2;       // softmax warps per (Q tile, TMEM lane quarter): each owns kN / kSplit keys
+#ifndef ELLM_PF_SPLIT
+#define ELLM_PF_SPLIT 1
+#endif
+constexpr int kSplit = ELLM_PF_SPLIT;  // softmax warps per (Q tile, TMEM lane quarter): each owns kN / kSplit keys
 constexpr int kSoftmaxWarps = 4 * kQTiles * kSplit;
 constexpr int kThreads = 64 + 32 * kSoftmaxWarps;  // warp 0 TMA, warp 1 MMA, 8 softmax warps per Q tile
 constexpr uint32_t kTmemCols = 512;
@@ -98,16 +101,10 @@ __device__ __forceinline__ float ex2(float x) {
 }
 // 2^x on the FMA / integer pipes (no MUFU): round-to-nearest split x = j + f, f in [-1/2, 1/2],
 // 2^f by a cubic (relative-error fit on [-1/2, 1/2]: < 7.5e-5, far below bf16's 2^-9 half-ulp
-// of P; checked in tests/test_prefill_exp2.py against numpy), then j added
-// to the exponent field. Inputs are clamped at -125 so the result stays a normal float (>= 2^-125.5;
-// masked scores, -inf, give that instead of 0 — 1e-38 of a zeroed or finite V row).
-__device__ __forceinline__ float ex2_fma(float x) {
-  x = fmaxf(x, -125.f);
-  const float r = x + 12582912.f;  // 1.5 * 2^23: the low mantissa bits of r hold round(x)
-  const float f = x - (r - 12582912.f);
-  const float q = fmaf(fmaf(fmaf(0.05517161f, f, 0.24261114f), f, 0.693261f), f, 0.99992807f);
-  return __int_as_float(__float_as_int(q) + (__float_as_int(r) << 23));
-}
+// of P; the arithmetic below is emulated in numpy and checked in tests/test_prefill_exp2.py), then
+// j added to the exponent field. Inputs are clamped at -125 so the result stays a normal float
+// (>= 2^-125.5; masked scores, -inf, give that instead of 0 — 1e-38 of a zeroed or finite V row).
+constexpr float kE2C3 = 0.05517161f, kE2C2 = 0.24261114f, kE2C1 = 0.693261f, kE2C0 = 0.99992807f;
 // sm_100 packed fp32 pairs (one FFMA2 / FADD2 instead of two FFMA / FADD: fewer issue slots)
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   uint64_t d;
@@ -122,17 +119,17 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
       : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
   return *reinterpret_cast<float2*>(&d);
 }
-// ex2_fma on a pair with packed fp32 ops (FADD2 / FFMA2: the same roundings as the scalar form,
-// x - (r - M) as an exact fma by -1): 12 instructions per two exponentials instead of ~20.
+// The FMA-pipe exp2 above on a pair with packed fp32 ops (FADD2 / FFMA2; x - (r - M) as an exact
+// fma by -1): 12 instructions per two exponentials.
 __device__ __forceinline__ float2 ex2_fma2(float2 x) {
   x.x = fmaxf(x.x, -125.f);
   x.y = fmaxf(x.y, -125.f);
   const float2 M = make_float2(12582912.f, 12582912.f), mM = make_float2(-12582912.f, -12582912.f);
   const float2 r = fadd2(x, M);
   const float2 f = ffma2(fadd2(r, mM), make_float2(-1.f, -1.f), x);
-  float2 q = ffma2(make_float2(0.05517161f, 0.05517161f), f, make_float2(0.24261114f, 0.24261114f));
-  q = ffma2(q, f, make_float2(0.693261f, 0.693261f));
-  q = ffma2(q, f, make_float2(0.99992807f, 0.99992807f));
+  float2 q = ffma2(make_float2(kE2C3, kE2C3), f, make_float2(kE2C2, kE2C2));
+  q = ffma2(q, f, make_float2(kE2C1, kE2C1));
+  q = ffma2(q, f, make_float2(kE2C0, kE2C0));
   return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(r.x) << 23)),
                      __int_as_float(__float_as_int(q.y) + (__float_as_int(r.y) << 23)));
 }
@@ -432,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int pos_idx = x * bp + row / g;
     const bool valid = pos_idx < n_valid;
     const int prow = valid ? p0 + pos_idx : p0;  // causal limit of this row
-    const uint32_t pair_bar = 1 + x * 4 + quarter;  // named barrier of the two halves' warps
+    [[maybe_unused]] const uint32_t pair_bar = 1 + x * 4 + quarter;  // named barrier of the split warps
     float* red = reinterpret_cast<float*>(smem + LY::off_red);
     auto red_at = [&](int par, int hh) -> float& { return red[((par * kQTiles + x) * kSplit + hh) * kM + row]; };
     if (x < nq) {
@@ -462,10 +459,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
         // exchange with the other half (parity-buffered: the partner is at most one tile apart);
         // the barrier also orders both halves' S loads before either overwrites S with P
-        red_at(t & 1, h) = m_half;
-        asm volatile("bar.sync %0, %1;" ::"r"(pair_bar), "n"(32 * kSplit) : "memory");
+        if constexpr (kSplit > 1) {
+          red_at(t & 1, h) = m_half;
+          asm volatile("bar.sync %0, %1;" ::"r"(pair_bar), "n"(32 * kSplit) : "memory");
+        }
         if (x == 0 && h == 0 && quarter == 0 && lane == 0) pf_stamp(p, t, 9);
-        const float m_tile = fmaxf(m_half, red_at(t & 1, h ^ 1)) * p.scale_log2;
+        const float m_tile = (kSplit > 1 ? fmaxf(m_half, red_at(t & 1, h ^ 1)) : m_half) * p.scale_log2;
         // lazy rescale: the reference max moves only when the tile max exceeds it by more than
         // the headroom (both halves see the same m_tile, so they decide alike); each warp
         // rescales its half of O_x's columns (tcgen05.ld/st are .aligned: warp-uniform branch)
@@ -529,9 +528,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(p_full + 8 * x);
       }
       // ---- epilogue: O_x / (l_h0 + l_h1) -> bf16 -> out[q_row0 + pos][kvh*group + head][h half] ----
-      red_at(n_tiles & 1, h) = l_run;
-      asm volatile("bar.sync %0, %1;" ::"r"(pair_bar), "n"(32 * kSplit) : "memory");
-      const float inv = 1.f / (l_run + red_at(n_tiles & 1, h ^ 1));
+      float l_other = 0.f;
+      if constexpr (kSplit > 1) {
+        red_at(n_tiles & 1, h) = l_run;
+        asm volatile("bar.sync %0, %1;" ::"r"(pair_bar), "n"(32 * kSplit) : "memory");
+        l_other = red_at(n_tiles & 1, h ^ 1);
+      }
+      const float inv = 1.f / (l_run + l_other);
       mbar_wait(o_full + 8 * x, 0);
       tc_fence_after();
       __nv_bfloat16* dst = p.out + (int64_t(q_row0 + pos_idx) * p.Hq + kvh * g + row % g) * D + h * (D / kSplit);
@@ -575,7 +578,7 @@ cudaError_t launch_de(const PrefillMaps& maps, const PParams& prm, int n_work, c
   return cudaGetLastError();
 }
 
-constexpr int kDefaultEmu = 0;  // measured: MUFU for all (1187 vs 1094 TFLOP/s at 2 x 4K over 32K)
+constexpr int kDefaultEmu = 1;  // 1 of every 4 pairs on the FMA pipe: +2-4% over 0 (tools/pf_split_emu.sh)
 template <int D>
 cudaError_t launch_d(const PrefillMaps& maps, const PParams& prm, int n_work, cudaStream_t s) {
   const char* v = std::getenv("ELLM_PF_EMU");  // measurement knob: 0, 1, 2 or 3 pairs of every 4
