@@ -238,7 +238,7 @@ __device__ __forceinline__ void pf_stamp(const PParams& p, int t, int k) {
 // first 64 columns — and O_x at [256 + 128x, 256 + 128x + D). Both tiles share every K/V tile.
 // The MMA thread issues, per key tile t:  PV_0(t), S_0(t+1), PV_1(t), S_1(t+1), so while softmax
 // warpgroup x works on S_x(t+1) the tensor pipe runs the other tile's P.V and S.
-// EMU: of every 4 pairs of softmax exponentials, this many run on the FMA pipe (ex2_fma2), the rest
+// EMU: of every 8 pairs of softmax exponentials, this many run on the FMA pipe (ex2_fma2), the rest
 // on MUFU
 template <int D, int EMU>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 32; j += 2) {
             const float2 y = ffma2(make_float2(xs[32 * c + j], xs[32 * c + j + 1]), sc2, nm2);
             float a, b;
-            if (((j >> 1) & 3) < EMU) {  // this pair on the FMA pipe
+            if ((((32 * c + j) >> 1) & 7) < EMU) {  // this pair on the FMA pipe
               const float2 e = ex2_fma2(y);
               a = e.x;
               b = e.y;
@@ -578,16 +578,16 @@ cudaError_t launch_de(const PrefillMaps& maps, const PParams& prm, int n_work, c
   return cudaGetLastError();
 }
 
-constexpr int kDefaultEmu = 1;  // 1 of every 4 pairs on the FMA pipe: +2-4% over 0 (tools/pf_split_emu.sh)
+constexpr int kDefaultEmu = 2;  // 2 of every 8 pairs on the FMA pipe: +2-4% over 0 (tools/pf_split_emu.sh)
 template <int D>
 cudaError_t launch_d(const PrefillMaps& maps, const PParams& prm, int n_work, cudaStream_t s) {
-  const char* v = std::getenv("ELLM_PF_EMU");  // measurement knob: 0, 1, 2 or 3 pairs of every 4
+  const char* v = std::getenv("ELLM_PF_EMU");  // measurement knob: 0, 1, 2 or 3 pairs of every 8
   const int emu = v ? std::atoi(v) : kDefaultEmu;
   switch (emu) {
+    case 0: return launch_de<D, 0>(maps, prm, n_work, s);
     case 1: return launch_de<D, 1>(maps, prm, n_work, s);
-    case 2: return launch_de<D, 2>(maps, prm, n_work, s);
     case 3: return launch_de<D, 3>(maps, prm, n_work, s);
-    default: return launch_de<D, 0>(maps, prm, n_work, s);
+    default: return launch_de<D, 2>(maps, prm, n_work, s);
   }
 }
 
