@@ -4,6 +4,7 @@
 //   chunk_copy      whole-chunk copies for deflate / inflate / migrate (a6-a8)
 // All three are HBM- (or host-link-) bound byte copies: 16-byte vector accesses, several
 // independent loads in flight per thread before the stores, grids sized to the SM count.
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include "internal.h"
@@ -255,12 +256,15 @@ cudaError_t launch_chunk_copy(uint8_t* dst_base, const int32_t* dst_idx, const u
   const bool want_bulk = bulk_e ? std::atoi(bulk_e) != 0 : pow2;
   if (src_dev && dst_dev && seg_off == 0 && seg_bytes == chunk_bytes && chunk_bytes % kBulkUnit == 0 &&
       (!rot || slab % kBulkUnit == 0) && want_bulk) {
-    static bool configured = false;
-    if (!configured) {
+    static std::atomic<uint64_t> configured{0};  // per device (function attributes are per context)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    if (!(configured.load(std::memory_order_acquire) & bit)) {
       cudaError_t e = cudaFuncSetAttribute(chunk_copy_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            kBulkSmem);
       if (e != cudaSuccess) return e;
-      configured = true;
+      configured.fetch_or(bit, std::memory_order_release);
     }
     const int64_t bunits = int64_t(n) * (chunk_bytes / kBulkUnit);
     const int64_t bneed = (bunits + kBulkGrab - 1) / kBulkGrab;

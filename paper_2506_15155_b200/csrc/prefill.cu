@@ -21,6 +21,7 @@
 //    mask, base-2 online softmax with lazy rescaling (O in TMEM is rescaled only when the row max
 //    grows by more than 2^8), P written as bf16 into shared memory in the swizzled K-major layout,
 //    and at the end O / l -> bf16 -> global.
+#include <atomic>
 #include <cstdlib>
 
 #include <cuda_bf16.h>
@@ -567,12 +568,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int D, int EMU>
 cudaError_t launch_de(const PrefillMaps& maps, const PParams& prm, int n_work, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};  // per device (function attributes are per context)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (!(configured.load(std::memory_order_acquire) & bit)) {
     cudaError_t e = cudaFuncSetAttribute(prefill_kernel<D, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Layout<D>::bytes);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured.fetch_or(bit, std::memory_order_release);
   }
   prefill_kernel<D, EMU><<<n_work, kThreads, Layout<D>::bytes, s>>>(maps, prm);
   return cudaGetLastError();
