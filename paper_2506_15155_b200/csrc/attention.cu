@@ -22,6 +22,7 @@
 //  * Each warp writes an fp32 partial (m, l, o) per (CTA, request); the last CTA to finish a
 //    request (per-request arrival counter) merges its partials with the log-sum-exp rule and
 //    writes the bf16 output, so one launch does rows a4 and a5.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -38,6 +39,7 @@ constexpr int kThreads = (kConsumerWarps + 1) * 32;
 __host__ __device__ constexpr int stages_for(int D) { return D == 128 ? 3 : 6; }
 __host__ __device__ constexpr int stage_bytes_for(int D) { return 2 * 128 * D * 2; }  // HB*TT = 128
 constexpr int kQSlots = 2;  // Q ring: one slot per in-flight (owner, request) segment
+constexpr int kL2PrefetchTiles = 6;  // default of Params::l2pf (set from measurements)
 __host__ __device__ constexpr int q_slot_bytes_for(int D) { return 8 * 8 * D * 2; }  // HB*group <= 64 rows
 __host__ __device__ constexpr int smem_bytes_for(int D) {
   return stages_for(D) * stage_bytes_for(D) + kQSlots * q_slot_bytes_for(D) + 1024 /*align*/ +
@@ -83,6 +85,13 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n}" ::"r"(bar), "r"(parity) : "memory");
+}
+// L2-only prefetch of one TMA box (no shared-memory destination, no completion)
+__device__ __forceinline__ void tma_prefetch_5d(const CUtensorMap* map, int c0, int c1, int c2, int c3, int c4) {
+  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+               : "memory");
 }
 __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
                                             int c3, int c4, uint32_t bar, uint64_t policy) {
@@ -172,6 +181,7 @@ struct Params {
   uint32_t gdone_target;
   unsigned long long* trace;  // ellm_set_attn_trace: [G][8] %globaltimer stamps of this launch, or null
   uint32_t range_shift;       // measurement knob: CTA i streams static range (i + shift) % G
+  int32_t l2pf;               // PDL / folded wait: tiles after the first NST prefetched into L2 before waiting
 };
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -486,6 +496,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int k = 0; k < 8; ++k) e[k] = __shfl_sync(0xffffffffu, ent[k], u);
             if (q_pending && issued == NST) {  // the ring is full: Q must be on its way
+              if (p.l2pf > 0 && !waited) {
+                // the previous launch's slowest CTAs still run: lanes u .. u+l2pf-1 prefetch the
+                // tiles after the ring's into L2 (their own entries), using the HBM bandwidth
+                // its tail leaves idle; the TMA loads then hit L2 (evict-first) after the wait
+                const int64_t tl = t + lane;
+                if (lane >= u && lane < cnt && lane < u + p.l2pf) {
+                  const int tokoff = int(((tl - tile0) * TT) % p.T);
+                  const int tok_in_chunk = p.T >= TT ? tokoff : 0;
+#pragma unroll
+                  for (int k = 0; k < 8; ++k)
+                    if (k < npieces && ent[k] >= 0)
+                      tma_prefetch_5d(&tmap, 0, 0, tok_in_chunk, hg * HB,
+                                      (ent[k] * p.L + slab_slot(ent[k], p.layer, p.rot)) * 2);
+                }
+                __syncwarp();
+              }
               pdl_wait();
               stage_q();
               q_pending = false;
@@ -980,6 +1006,15 @@ cudaError_t launch_paged_attention(const CUtensorMap& tmap, const AttnShape& sh,
   prm.gdone = plan.gdone;
   prm.trace = plan.trace;
   prm.range_shift = plan.range_shift;
+  {
+    // tiles prefetched into L2 while a launch waits on its predecessor (PDL) or on the peers'
+    // gather flags; ELLM_ATTN_L2PF overrides (0 = off)
+    static const int l2pf = [] {
+      const char* v = std::getenv("ELLM_ATTN_L2PF");
+      return v ? std::max(0, std::min(31, std::atoi(v))) : kL2PrefetchTiles;
+    }();
+    prm.l2pf = (plan.pdl || plan.wait_flag != nullptr) ? l2pf : 0;
+  }
   prm.gdone_target = plan.gdone_target;
   prm.wait_flag = plan.wait_flag;
   prm.wait_target = plan.wait_target;
