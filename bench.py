@@ -43,11 +43,16 @@ def parse():
                          "c5: 256-request prefill/decode churn with offload, compaction, shrink/grow")
     ap.add_argument("--swap-every", type=int, default=48,
                     help="c3: decode steps per offload/fetch round")
-    ap.add_argument("--swap-mode", choices=["sm", "ce", "mixed", "staged"], default="staged",
+    ap.add_argument("--swap-mode", choices=["sm", "ce", "mixed", "staged", "ctx"], default="ctx",
                     help="c3: swap with the SM copy kernels, the DMA copy engines, copy engines for "
-                         "swap-out and SM kernels for swap-in (mixed), or copy engines with a staged "
-                         "swap-in (host link -> staging buffer -> SM copy; the default: least "
-                         "interference with the decode, DESIGN.md §5 C3)")
+                         "swap-out and SM kernels for swap-in (mixed), copy engines with a staged "
+                         "swap-in (host link -> staging buffer -> SM copy), or copy engines with the "
+                         "swap-in through a second CUDA context's staging buffer (ctx, the default: "
+                         "least interference with the decode, DESIGN.md §5 C3)")
+    ap.add_argument("--c3-swapout", choices=["offload", "deflate"], default="offload",
+                    help="c3: swap-out by layer-wise offload with the commit deferred until the copy "
+                         "completed (default), or by deflate (frees the chunks at once, ordered after "
+                         "the copy: the decode's next chunk allocation then waits for it)")
     ap.add_argument("--resident", type=int, default=0,
                     help="c3: requests decoding in HBM (0 = as many as fit beside one in flight)")
     ap.add_argument("--gather", choices=["p2p", "nccl"], default="p2p",
@@ -299,7 +304,7 @@ def main():
     n_steps = args.warmup + args.steps
     e2e_steps = 0 if args.no_e2e else args.steps
     UNFUSED_STEPS = 3  # comparison: separate kv_append + attention launches
-    CONC_STEPS = 30 if swap_chunks else 0  # decode steps with a concurrent swap stream (15 per mode)
+    CONC_STEPS = 45 if swap_chunks else 0  # decode steps with a concurrent swap stream (15 per mode)
     e2e_steps += CONC_STEPS
     e2e_steps += UNFUSED_STEPS
     # distinct per-step inputs in a ring capped at ~2 GiB (the 70B shape's 105 MB per step would
@@ -489,14 +494,14 @@ def main():
     if swap_chunks:
         conc = {}
         c_first = n_steps + n_e2e
-        for mode, name in ((1, "ce"), (0, "sm")):
+        for mi, (mode, name) in enumerate(((1, "ce"), (3, "ctx"), (0, "sm"))):
             pool.set_swap_mode(mode)
             ss = torch.cuda.Stream()
             barrier()
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            half = CONC_STEPS // 2  # consecutive positions per mode
-            base = c_first + (0 if mode == 1 else half)
+            half = CONC_STEPS // 3  # consecutive positions per mode
+            base = c_first + mi * half
             d0.record(stream)  # decode first (the compute stream is busy ~half*20 ms) ...
             for s in range(base, base + half):
                 step(*inputs[s])
@@ -754,8 +759,8 @@ def run_c3(args):
     t_create = time.perf_counter() - t0
     cs = torch.cuda.current_stream()
     sp = cs.cuda_stream
-    out_mode = 0 if args.swap_mode == "sm" else 1
-    in_mode = {"ce": 1, "staged": 2}.get(args.swap_mode, 0)
+    out_mode = {"sm": 0, "ctx": 3}.get(args.swap_mode, 1)
+    in_mode = {"ce": 1, "staged": 2, "ctx": 3}.get(args.swap_mode, 0)
     pool.set_swap_mode(out_mode)
     # placement: requests R+1.. are prefilled through the pool and offloaded; 0..R stay
     host_q = []
@@ -777,11 +782,49 @@ def run_c3(args):
     NIN = 8  # input ring: Q / new K,V of the R decode slots for 8 steps (synthetic values)
     inputs = [W.decode_inputs(slot_wl, s, np.full(R, wl.context + s, np.int64)) for s in range(NIN)]
     out = torch.empty((L, R, Hq, d), dtype=torch.bfloat16, device="cuda")
-    attn_ev, swap_ev, swap_bytes = [], [], []
+    attn_ev, swap_ev, swap_bytes, swap_mid = [], [], [], []
     tokens = {r: 0 for r in range(total)}
 
-    def transition():
+    # Swap-out: by default the request's chunks are copied out with the layer-wise
+    # offload calls (offload_begin / offload_layer; the chunks stay USED and readable) and only
+    # committed — tables repointed to the host slots, chunks freed — once the copy has completed
+    # (polled at step boundaries). A deflate frees them at once instead, ordered after its copy:
+    # the decode's next kv_reserve then takes the lowest free chunk, one of those being copied
+    # out, and the compute stream waits for the whole 16 GiB copy-out (stream-ordered reuse, R7).
+    pending = None  # (x, ids, slots, e0, em): swap-out copy in flight, commit not yet issued
+
+    def swap_in_next(x, slots, e0, em):
         nonlocal incoming, in_ev
+        host_q.append((x, slots))
+        y, yslots = host_q.pop(0)
+        pool.set_swap_mode(in_mode)
+        e2, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e2.record(sw)                          # swap-in starts
+        rc, _ = pool.inflate(yslots, sw.cuda_stream)
+        if rc:
+            raise ellm.EllmError(rc, "c3 inflate")
+        e1.record(sw)
+        in_ev, incoming = e1, y
+        swap_ev.append((e0, e1))
+        swap_mid.append((em, e2))
+        swap_bytes.append(2 * len(slots) * pool.chunk_bytes)
+
+    def finish_swap_out(block=False):
+        nonlocal pending
+        if pending is None or not (block or pending[4].query()):
+            return
+        x, ids, slots, e0, em = pending
+        pending = None
+        if block:
+            em.synchronize()
+        rc = pool.offload_commit(ids, sw.cuda_stream)
+        if rc:
+            raise ellm.EllmError(rc, "c3 offload_commit")
+        swap_in_next(x, slots, e0, em)
+
+    def transition():
+        nonlocal incoming, in_ev, pending
+        finish_swap_out(block=True)            # (the previous round's, if still open)
         ev = torch.cuda.Event()
         ev.record(cs)
         sw.wait_event(ev)                      # X's last attention reads are done
@@ -789,25 +832,34 @@ def run_c3(args):
         if in_ev is not None:
             cs.wait_event(in_ev)               # the fetched request's bytes have landed
         D.append(incoming)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0, em = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(sw)
         ids = pool.table(x)[0].tolist()
         pool.set_swap_mode(out_mode)
-        rc, slots = pool.deflate(ids, sw.cuda_stream)
+        if args.c3_swapout == "deflate":
+            rc, slots = pool.deflate(ids, sw.cuda_stream)
+            if rc:
+                raise ellm.EllmError(rc, "c3 deflate")
+            em.record(sw)
+            swap_in_next(x, slots, e0, em)
+            return
+        rc, slots = pool.offload_begin(ids)
         if rc:
-            raise ellm.EllmError(rc, "c3 deflate")
-        host_q.append((x, slots))
-        y, yslots = host_q.pop(0)
-        pool.set_swap_mode(in_mode)
-        rc, _ = pool.inflate(yslots, sw.cuda_stream)
-        if rc:
-            raise ellm.EllmError(rc, "c3 inflate")
-        e1.record(sw)
-        in_ev, incoming = e1, y
-        swap_ev.append((e0, e1))
-        swap_bytes.append((len(ids) + len(yslots)) * pool.chunk_bytes)
+            raise ellm.EllmError(rc, "c3 offload_begin")
+        for l in range(L):
+            rc = pool.offload_layer(l, ids, sw.cuda_stream)
+            if rc:
+                raise ellm.EllmError(rc, "c3 offload_layer")
+        em.record(sw)                          # swap-out copy done
+        pending = (x, ids, slots, e0, em)
+
+    step_end = []  # per-step end events: the host runs at most LOOKAHEAD steps ahead of the GPU
+    LOOKAHEAD = 3
 
     def step(s, record=False, host=None):
+        if len(step_end) >= LOOKAHEAD:
+            step_end.pop(0).synchronize()
+        finish_swap_out()
         if s and s % args.swap_every == 0:
             transition()
         q, k, v = inputs[s % NIN] if host is None else host
@@ -828,6 +880,9 @@ def run_c3(args):
                 a1 = torch.cuda.Event(enable_timing=True)
                 a1.record(cs)
                 attn_ev.append((a0, a1, lens_now))
+        se = torch.cuda.Event()
+        se.record(cs)
+        step_end.append(se)
 
     s_glob = 0
     for _ in range(args.warmup):
@@ -854,11 +909,27 @@ def run_c3(args):
     attn_ms = [a.elapsed_time(b) for a, b, _ in attn_ev]
     alg = [sum(lens) * Hkv * d * 4 + 2 * R * Hq * d * 2 + 4 * sum((n + T - 1) // T for n in lens)
            for _, _, lens in attn_ev]
+    # decode steps by what the swap stream was doing meanwhile (times relative to ev0): a step is
+    # [first launch start, last launch end]; it counts as "out" / "in" if it overlaps a swap-out /
+    # swap-in phase of a timed round by more than half its length
+    phases = []
+    for (a, b), (m, m2) in zip(timed_swaps, swap_mid[n_swaps0:]):
+        t0, tm, tm2, t1 = ev0.elapsed_time(a), ev0.elapsed_time(m), ev0.elapsed_time(m2), ev0.elapsed_time(b)
+        phases += [("out", t0, tm), ("in", tm2, t1)]
+    by_phase = {"out": [], "in": [], "none": []}
+    for j in range(0, len(attn_ev) - L + 1, L):
+        s0, s1 = ev0.elapsed_time(attn_ev[j][0]), ev0.elapsed_time(attn_ev[j + L - 1][1])
+        ph = "none"
+        for nm, p0, p1 in phases:
+            if min(s1, p1) - max(s0, p0) > 0.5 * (s1 - s0):
+                ph = nm
+        by_phase[ph].append(s1 - s0)
     attn_mean = statistics.mean(attn_ms)
     achieved = statistics.mean(alg) / (attn_mean / 1e3) / 1e9
     peak, peak_src = hbm_peak()
 
     # the same resident set without swapping (isolated decode), and end to end through host buffers
+    finish_swap_out(block=True)  # no swap work left in flight for the isolated steps
     torch.cuda.synchronize()
     if in_ev is not None:
         in_ev.synchronize()
@@ -904,7 +975,7 @@ def run_c3(args):
             "data": "synthetic (seeded counter-based generator, 3 needles per request/layer/kv-head)",
             "config": {**workload_config(wl, 1), "resident_requests": R, "host_requests": total - R - 1,
                        "in_flight_requests": 1, "swap_every_steps": args.swap_every,
-                       "swap_mode": args.swap_mode, "pool_gib": round(regions * req_bytes / 2 ** 30, 1),
+                       "swap_mode": args.swap_mode, "swap_out": args.c3_swapout, "pool_gib": round(regions * req_bytes / 2 ** 30, 1),
                        "host_slots_gib": round(host_reqs * req_bytes / 2 ** 30, 1)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": None,
@@ -915,6 +986,10 @@ def run_c3(args):
             "c3": {"isolated_decode_ms_per_step": round(iso_ms, 4),
                    "swap_overhead_frac": round(1 - iso_ms / (el_ms / args.steps), 4),
                    "swaps_timed": len(timed_swaps),
+                   "decode_ms_per_step_by_swap_phase": {k: {"steps": len(v), "mean_ms": round(statistics.mean(v), 3) if v else None}
+                                                        for k, v in by_phase.items()},
+                   "swap_out_ms": [round(b - a, 1) for _, a, b in phases[0::2]],
+                   "swap_in_ms": [round(b - a, 1) for _, a, b in phases[1::2]],
                    "swap_round_ms": [round(x, 1) for x in swap_ms],
                    "swap_gbs_bidir_serial": [round(x, 2) for x in swap_gbs],
                    "bytes_per_swap_round": swap_bytes[-1] if swap_bytes else 0,
@@ -1110,7 +1185,7 @@ def measure_swap(pool, wl, stream):
         return e0.elapsed_time(e1) / 1e3, r
 
     res = {}
-    for mode, name in ((0, "sm"), (1, "ce")):
+    for mode, name in ((0, "sm"), (1, "ce"), (3, "ctx")):
         pool.set_swap_mode(mode)
         best_d2h, best_h2d, best_mig = 0.0, 0.0, 0.0
         for _ in range(3):

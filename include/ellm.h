@@ -368,8 +368,14 @@ int ellm_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
  * cudaMemcpyAsync per maximal contiguous run of the chunk list, one cudaMemcpy2DAsync per maximal
  * evenly strided run), 2 = as 1 for deflate / offload, and a staged inflate: the
  * host link writes 256 MiB batches into a device staging buffer outside the KV pool, then an SM
- * copy moves them into the chunks (inbound PCIe writes slow a concurrent decode more than
- * device-side writes, DESIGN.md §5 C3). All are exact byte copies. INVALID_ARG outside 0..2. */
+ * copy moves them into the chunks, 3 = as 1 for deflate / offload, and inflate through a second
+ * CUDA context on the pool's device, created by this call: 256 MiB batches host -> a staging
+ * buffer allocated by that context -> device-to-device into the chunks, all issued from it on its
+ * own stream, ordered against the caller's stream by events (host-link writes into memory of the
+ * decode's own context slow a concurrent decode ~2x; into another context's memory ~1.1x:
+ * DESIGN.md §5 C3). All are exact byte copies. INVALID_ARG outside 0..3; mode 3 returns CUDA
+ * (ellm_last_cuda_error = 10000 + CUresult for a driver failure) or UNSUPPORTED if the side
+ * context cannot be created. */
 int ellm_set_swap_mode(ellm_pool* pool, int32_t mode);
 
 /* ---- introspection (parity tests) --------------------------------------------------- */

@@ -36,6 +36,16 @@ struct Driver {
                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 };
 const Driver& driver();  // loads once; .ok false if unavailable
+// Context entry points for the swap engine's side context (swap mode 3): cuCtxCreate_v2 etc.
+struct CtxDriver {
+  bool ok = false;
+  CUresult (*deviceGet)(CUdevice*, int);
+  CUresult (*ctxCreate)(CUcontext*, unsigned int, CUdevice);
+  CUresult (*ctxDestroy)(CUcontext);
+  CUresult (*ctxPushCurrent)(CUcontext);
+  CUresult (*ctxPopCurrent)(CUcontext*);
+};
+const CtxDriver& ctx_driver();
 
 int64_t now_ns();
 int vt_unmap_slot_nosync(ellm_vtensor* vt, int64_t slot);
@@ -262,7 +272,13 @@ struct ellm_pool {
   ellm::AttnShape ash{};
   int num_sms = 0;
   ellm::StagingRing ring;
-  int swap_mode = 0;                 // 0 SM copy kernel, 1 copy engines, 2 staged inflate
+  int swap_mode = 0;                 // 0 SM copy kernel, 1 copy engines, 2 staged inflate, 3 side-context inflate
+  CUcontext side_ctx = nullptr;      // swap_mode 3: second context on the pool's device (copy engines)
+  cudaStream_t side_stream = nullptr;  // ... its stream
+  cudaEvent_t side_before = nullptr;   // recorded on the caller's stream (pool's context)
+  cudaEvent_t side_after = nullptr;    // recorded on side_stream (side context)
+  uint8_t* side_stage = nullptr;       // side context's staging buffer for inflate (256 MiB)
+  int64_t side_stage_chunks = 0;
   uint8_t* d_stage = nullptr;        // swap_mode 2: device staging buffer for inflate (256 MiB)
   cudaEvent_t stage_ev = nullptr;    // last use of the staging buffer
   cudaStream_t stage_stream = nullptr;

@@ -166,6 +166,93 @@ cudaError_t ce_copy(uint8_t* dst_base, const std::vector<int32_t>& dst, const ui
   return issue_copies(pc, stream);
 }
 
+// Swap mode 3: inflate through a second CUDA context on the pool's device. Measured
+// (tools/interference_ctx2.py, DESIGN.md §5 C3): a concurrent 128 GiB decode step slows 2.33x
+// while host -> device copies land in memory allocated by the decode's own context, 1.67x when
+// another context issues them into that memory, but only 1.08x when they land in memory
+// allocated by the other context — and 1.08x also when that context then moves the data on into
+// the decode's memory with device -> device copies. So inflate copies each batch of up to 256 MiB
+// from the host slots into a staging buffer owned by the side context, then device -> device
+// into the chunks (copy engines, issued from the side context, canonical -> rotated slabs as in
+// ce_copy). Stream order is kept with two events: the side stream waits for the caller's prior
+// work, the caller's stream waits for the copies. The pool VA (VMM, mapped process-wide and
+// granted to the device) and the portable pinned host slots are addressable from the side
+// context. Driver failures are reported as ELLM_ERR_CUDA with last_cuda_error = 10000 + CUresult.
+constexpr int64_t kSideStageBytes = int64_t(256) << 20;
+void side_destroy(ellm_pool* p);
+int side_init(ellm_pool* p) {
+  if (p->side_ctx) return ELLM_OK;
+  const CtxDriver& d = ctx_driver();
+  if (!d.ok) return ELLM_ERR_UNSUPPORTED;
+  CUdevice dev;
+  CUcontext c = nullptr, prev = nullptr;
+  CUresult r = d.deviceGet(&dev, p->cfg.device);
+  if (r == CUDA_SUCCESS) r = d.ctxCreate(&c, 0, dev);
+  if (r != CUDA_SUCCESS) {
+    p->last_cuda_error = 10000 + int(r);
+    return ELLM_ERR_CUDA;
+  }
+  // cuCtxCreate made `c` current: the runtime calls below create its stream, event and buffer
+  const int64_t stage = std::max<int64_t>(1, kSideStageBytes / p->chunk_bytes) * p->chunk_bytes;
+  cudaError_t e = cudaStreamCreateWithFlags(&p->side_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->side_after, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&p->side_stage), size_t(stage));
+  d.ctxPopCurrent(&prev);
+  p->side_ctx = c;
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->side_before, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    const int rc = cuda_fail(p, e);
+    side_destroy(p);
+    return rc;
+  }
+  p->side_stage_chunks = stage / p->chunk_bytes;
+  return ELLM_OK;
+}
+void side_destroy(ellm_pool* p) {
+  if (!p->side_ctx) return;
+  const CtxDriver& d = ctx_driver();
+  if (d.ctxPushCurrent(p->side_ctx) == CUDA_SUCCESS) {
+    if (p->side_stream) {
+      cudaStreamSynchronize(p->side_stream);
+      cudaStreamDestroy(p->side_stream);
+    }
+    if (p->side_after) cudaEventDestroy(p->side_after);
+    if (p->side_stage) cudaFree(p->side_stage);
+    CUcontext prev;
+    d.ctxPopCurrent(&prev);
+  }
+  if (p->side_before) cudaEventDestroy(p->side_before);
+  d.ctxDestroy(p->side_ctx);
+  p->side_ctx = nullptr;
+  p->side_stream = nullptr;
+  p->side_after = p->side_before = nullptr;
+  p->side_stage = nullptr;
+}
+// pool chunks dst[i] <- host slots src[i] through the side context's staging buffer
+cudaError_t side_inflate_copy(ellm_pool* p, uint8_t* pool, const std::vector<int32_t>& dst,
+                              const std::vector<int32_t>& src, cudaStream_t stream) {
+  const CtxDriver& d = ctx_driver();
+  cudaError_t e = cudaEventRecord(p->side_before, stream);
+  if (e != cudaSuccess) return e;
+  if (d.ctxPushCurrent(p->side_ctx) != CUDA_SUCCESS) return cudaErrorContextIsDestroyed;
+  e = cudaStreamWaitEvent(p->side_stream, p->side_before, 0);
+  const int64_t S_chunks = p->side_stage_chunks;
+  for (size_t b0 = 0; b0 < dst.size() && e == cudaSuccess; b0 += size_t(S_chunks)) {
+    const size_t k = std::min(dst.size() - b0, size_t(S_chunks));
+    std::vector<int32_t> sidx(k), hs(src.begin() + int64_t(b0), src.begin() + int64_t(b0 + k)),
+        ds(dst.begin() + int64_t(b0), dst.begin() + int64_t(b0 + k));
+    for (size_t i = 0; i < k; ++i) sidx[i] = int32_t(i);
+    e = ce_copy(p->side_stage, sidx, p->host_slots, hs, p->chunk_bytes, p->side_stream);  // host link
+    if (e == cudaSuccess)  // canonical staging image -> (rotated) chunk slabs
+      e = ce_copy(pool, ds, p->side_stage, sidx, p->chunk_bytes, p->side_stream, p->ash.rot, p->ash.slab, 2);
+  }
+  if (e == cudaSuccess) e = cudaEventRecord(p->side_after, p->side_stream);
+  CUcontext prev;
+  d.ctxPopCurrent(&prev);
+  if (e != cudaSuccess) return e;
+  return cudaStreamWaitEvent(stream, p->side_after, 0);
+}
+
 // ---- stream-ordered reuse of freed chunks / host slots (see ellm_pool::FreeEvent) ----------
 // Record an event on `stream` after the work that frees some chunks / slots; returns its index.
 int32_t record_free_event(ellm_pool* p, cudaStream_t stream) {
@@ -629,6 +716,7 @@ int ellm_pool_destroy(ellm_pool* p) {
     if (p->d_table) cudaFree(p->d_table);
     if (p->d_stage) cudaFree(p->d_stage);
     if (p->stage_ev) cudaEventDestroy(p->stage_ev);
+    side_destroy(p);
     if (p->d_part) cudaFree(p->d_part);
     if (p->d_part_ml) cudaFree(p->d_part_ml);
     if (p->d_arrivals) cudaFree(p->d_arrivals);
@@ -680,7 +768,12 @@ void* ellm_pool_base(const ellm_pool* p) { return p && p->vt ? ellm_vtensor_base
 void* ellm_pool_host_base(const ellm_pool* p) { return p ? p->host_slots : nullptr; }
 
 int ellm_set_swap_mode(ellm_pool* p, int32_t mode) {
-  if (!p || mode < 0 || mode > 2) return ELLM_ERR_INVALID_ARG;
+  if (!p || mode < 0 || mode > 3) return ELLM_ERR_INVALID_ARG;
+  if (mode == 3 && p->has_dev) {
+    if (cudaSetDevice(p->cfg.device) != cudaSuccess) return ELLM_ERR_CUDA;
+    const int rc = side_init(p);
+    if (rc) return rc;
+  }
   p->swap_mode = mode;
   return ELLM_OK;
 }
@@ -1289,7 +1382,9 @@ int ellm_inflate(ellm_pool* p, int32_t n, const int32_t* slots, int32_t* ids_out
   for (int32_t c : dst)  // a chunk freed by work on another stream
     if ((e = wait_freed(p, p->chunk_ev, c, S(stream))) != cudaSuccess) return cuda_fail(p, e);
   uint8_t* pool = static_cast<uint8_t*>(ellm_vtensor_base(p->vt));
-  if (p->swap_mode == 1) {
+  if (p->swap_mode == 3) {
+    if ((e = side_inflate_copy(p, pool, dst, src, S(stream))) != cudaSuccess) return cuda_fail(p, e);
+  } else if (p->swap_mode == 1) {
     if ((e = ce_copy(pool, dst, p->host_slots, src, p->chunk_bytes, S(stream), p->ash.rot, p->ash.slab, 2)) !=
         cudaSuccess)
       return cuda_fail(p, e);

@@ -1,5 +1,6 @@
 // vmm.cpp — driver VMM entry points, the vtensor (the paper's eTensor) and the
 // staging ring used to snapshot host metadata into stream-ordered device uploads.
+#include <dlfcn.h>
 #include <time.h>
 
 #include <algorithm>
@@ -43,6 +44,31 @@ const Driver& driver() {
     ok &= load_sym("cuMemSetAccess", d.memSetAccess);
     ok &= load_sym("cuMemGetAllocationGranularity", d.memGetAllocationGranularity);
     ok &= load_sym("cuTensorMapEncodeTiled", d.tensorMapEncodeTiled);
+    d.ok = ok;
+  });
+  return d;
+}
+
+// The context calls by their explicit ABI names from the driver library itself (the unversioned
+// entry-point query can resolve "cuCtxCreate" to a later ABI with a different signature).
+template <typename F>
+static bool load_drv(void* lib, const char* name, F& fn) {
+  void* p = lib ? dlsym(lib, name) : nullptr;
+  fn = reinterpret_cast<F>(p);
+  return p != nullptr;
+}
+
+const CtxDriver& ctx_driver() {
+  static CtxDriver d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* lib = dlopen("libcuda.so.1", RTLD_NOW | RTLD_LOCAL);
+    bool ok = lib != nullptr;
+    ok &= load_drv(lib, "cuDeviceGet", d.deviceGet);
+    ok &= load_drv(lib, "cuCtxCreate_v2", d.ctxCreate);
+    ok &= load_drv(lib, "cuCtxDestroy_v2", d.ctxDestroy);
+    ok &= load_drv(lib, "cuCtxPushCurrent_v2", d.ctxPushCurrent);
+    ok &= load_drv(lib, "cuCtxPopCurrent_v2", d.ctxPopCurrent);
     d.ok = ok;
   });
   return d;

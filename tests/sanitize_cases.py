@@ -26,8 +26,8 @@ def case_c1():
     lens = [17, 64, 129, 300]
     assert t.reserve([0, 1, 2, 3], lens) == 0
     t.append_all_layers([0, 1, 2, 3], lens)
-    for mode in (0, 1, 2):
-        t.p.set_swap_mode(mode)
+    for mode in (0, 1, 2, 3):
+        assert t.p.set_swap_mode(mode) == 0
         rc, slots = t.deflate(t.o.table(3)[0][:8].tolist())
         assert rc == 0
         assert t.inflate(slots)[0] == 0

@@ -145,10 +145,10 @@ def test_elastic_ops_bytes_and_attention():
             t.attention(l, resident)
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
 def test_swap_modes_roundtrip(mode):
     t = Twin(2, 32, 8, 128, 16, 40, 40, 3, 12, 40, seed=2)
-    t.p.set_swap_mode(mode)
+    assert t.p.set_swap_mode(mode) == 0, t.p.last_cuda_error()
     assert t.reserve([0, 1, 2], [100, 60, 150]) == 0
     t.append_all_layers([0, 1, 2], [100, 60, 150])
     before = t.attention(1, [0, 1, 2])[1][0]

@@ -29,13 +29,14 @@ def test_rotated_slabs_match_oracle(rotate, bulk, monkeypatch):
     t.check_bytes()
     for l in range(L):
         t.attention(l, list(range(R)))
-    # swap-out with the SM copy kernel, swap-in with the copy engines (and the reverse)
-    for out_mode, in_mode, r in ((0, 1, 2), (1, 0, 4)):
-        t.p.set_swap_mode(out_mode)
+    # swap-out with the SM copy kernel, swap-in with the copy engines (and the reverse), and both
+    # through the copy engines of the side context (swap mode 3)
+    for out_mode, in_mode, r in ((0, 1, 2), (1, 0, 4), (3, 3, 5)):
+        assert t.p.set_swap_mode(out_mode) == 0
         rc, slots = t.deflate(t.o.table(r)[0].tolist()[::-1])
         assert rc == 0
         t.check_bytes()
-        t.p.set_swap_mode(in_mode)
+        assert t.p.set_swap_mode(in_mode) == 0
         assert t.inflate(slots[::2])[0] == 0
         assert t.inflate(slots[1::2])[0] == 0
         t.check_tables()

@@ -32,13 +32,17 @@ def _check_chunk(img, wl, r, i, T=16):
             assert np.array_equal(img[l, kv].transpose(1, 0, 2), want), (r, i, l, kv)
 
 
-def test_deflate_then_reuse_on_another_stream():
+@pytest.mark.parametrize("mode", [0, 3])
+def test_deflate_then_reuse_on_another_stream(mode):
+    """mode 0: SM copy kernels; mode 3: copy engines of the pool's side context (the copies run
+    on another context's stream, ordered by events)."""
     import torch
     from inputs import workload as W
     from paper_2506_15155_b200 import ellm
     wl = W.Workload("streams", 32, 32, 8, 128, 2, 32000, seed=9, needle=False)
     n_chunks = 2000
     pool = ellm.Pool(0, 32, 32, 8, 128, 16, 2 * n_chunks + 8, 2 * n_chunks + 8, 2, n_chunks, n_chunks)
+    assert pool.set_swap_mode(mode) == 0, pool.last_cuda_error()
     s0, s1, s2 = torch.cuda.current_stream(), torch.cuda.Stream(), torch.cuda.Stream()
     assert pool.reserve([0], [wl.context], s0.cuda_stream) == 0
     _fill(pool, wl, 0, wl.context, s0)
@@ -67,4 +71,30 @@ def test_deflate_then_reuse_on_another_stream():
     for i in (0, 1234, n_chunks - 1):
         _check_chunk(pool.read_chunk(int(ids_back[i])), wl, 0, i)
         _check_chunk(pool.read_host_slot(int(slots_b[i])), wl, 1, i)
+    pool.close()
+
+
+def test_side_context_copies_follow_the_callers_stream():
+    """Swap mode 3 on ONE stream with no host synchronisation: the side context's copy-out must
+    start after the appends queued before it, and the work queued after an inflate (an append
+    into the same request, then a read-back) must wait for the copy-in."""
+    import torch
+    from inputs import workload as W
+    from paper_2506_15155_b200 import ellm
+    wl = W.Workload("streams3", 32, 32, 8, 128, 2, 16000, seed=11, needle=False)
+    n_chunks = 1000
+    pool = ellm.Pool(0, 32, 32, 8, 128, 16, n_chunks + 8, n_chunks + 8, 2, n_chunks + 1, n_chunks)
+    assert pool.set_swap_mode(3) == 0, pool.last_cuda_error()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        assert pool.reserve([0], [wl.context], s.cuda_stream) == 0
+        _fill(pool, wl, 0, wl.context, s)               # ~2 GiB of appends, still running
+        rc, slots = pool.deflate(pool.table(0)[0].tolist(), s.cuda_stream)
+        assert rc == 0
+        rc, ids = pool.inflate(slots, s.cuda_stream)   # back into (other) chunks
+        assert rc == 0
+    s.synchronize()
+    for i in (0, 500, n_chunks - 1):
+        _check_chunk(pool.read_host_slot(int(slots[i])), wl, 0, i)   # copied out after the appends
+        _check_chunk(pool.read_chunk(int(ids[i])), wl, 0, i)          # copied in before the read
     pool.close()
