@@ -512,6 +512,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         l_run += ((sm[0].x + sm[0].y) + (sm[1].x + sm[1].y)) + ((sm[2].x + sm[2].y) + (sm[3].x + sm[3].y));
         if (x == 0 && h == 0 && t == n_tiles - 1) {  // V rows past the last visible key may hold anything
           const int need = last_key + 1 - t * kN;
+          // after the tile's TMA has landed: its last chunk piece may cover rows >= need, and S(t)
+          // complete does not imply V(t) complete (V is loaded one tile behind K)
+          mbar_wait(v_full + 8 * (t % kVStages), (t / kVStages) & 1);
           if (row >= need) {
             uint8_t* vrow = smem + LY::off_v + (t % kVStages) * LY::TILE + row * 128;
 #pragma unroll
