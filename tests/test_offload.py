@@ -63,19 +63,20 @@ def test_offload_commit_needs_every_layer_not_a_count():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode,rotate", [(0, "0"), (1, "0"), (0, "1"), (1, "1")])
+@pytest.mark.parametrize("mode,rotate", [(0, "0"), (1, "0"), (0, "1"), (1, "1"), (3, "1")])
 def test_offload_layerwise_bytes_overlapped_with_appends(mode, rotate, monkeypatch):
     """Prefill request 1 layer by layer on the compute stream while each finished layer is
     offloaded on a second stream (event per layer); after commit the host slots hold exactly
-    what the oracle's deflate holds. SM copy kernel (mode 0) or copy engines (mode 1), canonical
-    or rotated slabs (request 1's chunks sit in the second rotation group)."""
+    what the oracle's deflate holds. SM copy kernel (mode 0) or copy engines (mode 1; mode 3 adds
+    the fetch-back through the side context), canonical or rotated slabs (request 1's chunks sit
+    in the second rotation group)."""
     import torch
     from inputs import gen
     from tests.twin import Twin, bits_to_torch
     monkeypatch.setenv("ELLM_ROTATE", rotate)
     L, Hq, Hkv, d, T = 4, 32, 8, 128, 16
     t = Twin(L, Hq, Hkv, d, T, 64, 64, 2, 40, 32, seed=17)
-    t.p.set_swap_mode(mode)
+    assert t.p.set_swap_mode(mode) == 0
     assert t.reserve([0, 1], [600, 300]) == 0
     t.append_all_layers([0], [600])
     ids = t.p.table(1)[0].tolist()
