@@ -338,7 +338,8 @@ def main():
     sp = stream.cuda_stream
     attn_ev, app_ev, reserve_s = [], [], []
 
-    def step(q, k, v, record=False, fused=True):
+    def step(q, k, v, record=False, fused=True, o=None):
+        o = out if o is None else o
         t0 = time.perf_counter()
         rc = pool.reserve(reqs, ones, sp)
         if record:
@@ -362,7 +363,7 @@ def main():
                             raise ellm.EllmError(rc, "gather_wait_next")
                     rc = pool.attention_gather(l, reqs, q[l], pg.offset(l), scale, k[l], v[l], sp)
                 else:
-                    rc = pool.decode_append_attention(l, reqs, k[l], v[l], q[l], out[l], scale, sp)
+                    rc = pool.decode_append_attention(l, reqs, k[l], v[l], q[l], o[l], scale, sp)
                 if rc:
                     raise ellm.EllmError(rc, "decode_append_attention")
             else:
@@ -379,7 +380,7 @@ def main():
                 if pg is not None:
                     rc = pool.attention_gather(l, reqs, q[l], pg.offset(l), scale, None, None, sp)
                 else:
-                    rc = pool.attention(l, reqs, q[l], out[l], scale, sp)
+                    rc = pool.attention(l, reqs, q[l], o[l], scale, sp)
                 if rc:
                     raise ellm.EllmError(rc, "attention")
             if pg is not None and (l == L - 1 or not fused):  # the step's result: every rank's rows
@@ -391,7 +392,7 @@ def main():
                 e1.record(stream)
                 attn_ev.append((e0, e1, L if span else 1))
             if gath is not None:
-                dist.all_gather_into_tensor(gath[l], out[l])
+                dist.all_gather_into_tensor(gath[l], o[l])
 
     def barrier():
         torch.cuda.synchronize()
@@ -457,26 +458,56 @@ def main():
         hin = _Ring()
         for s in range(n_steps, n_steps + min(n_e2e, n_ring)):
             hin.append(tuple(x.cpu().pin_memory() for x in inputs[s]))
-        dq, dk, dv = (torch.empty_like(x) for x in inputs[0])
+        # Pipelined: step j+1's inputs are copied up on a second stream while step
+        # j runs, and step j's result is read back on a third stream; inputs and outputs
+        # double-buffered. (Measured, tools/e2e_probe.py: plain copies beat ellm_upload's
+        # side-context staging here — these footprints / upload sizes see little interference.)
+        dev_in = [tuple(torch.empty_like(x) for x in inputs[0]) for _ in range(2)]
         if pg is not None:  # the result of a step is the gathered [L, B, Hq, d] output
-            hout = torch.empty(L * pg.stride, dtype=torch.uint8).pin_memory()
+            hout = [torch.empty(L * pg.stride, dtype=torch.uint8).pin_memory() for _ in range(2)]
+            outs = [out, out]  # the gather window is the output (one per rank, reused per step)
         else:
-            hout = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+            hout = [torch.empty(out.shape, dtype=out.dtype).pin_memory() for _ in range(2)]
+            outs = [out, torch.empty_like(out)]
         h2d = sum(x.numel() * x.element_size() for x in hin[0])
-        d2h = hout.numel() * hout.element_size()
+        d2h = hout[0].numel() * hout[0].element_size()
+        up, dn = torch.cuda.Stream(), torch.cuda.Stream()
+        ev_up, ev_used, ev_dl = [None, None], [None, None], [None, None]
+
+        def upload(j):
+            b = j % 2
+            if ev_used[b] is not None:
+                up.wait_event(ev_used[b])  # step j-2 has consumed this input set
+            with torch.cuda.stream(up):
+                for dt, ht in zip(dev_in[b], hin[j]):
+                    dt.copy_(ht, non_blocking=True)
+            ev_up[b] = torch.cuda.Event()
+            ev_up[b].record(up)
+
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        up.wait_event(e0)
+        upload(0)
         for j in range(n_e2e):
-            hq, hk, hv = hin[j]
-            dq.copy_(hq, non_blocking=True)
-            dk.copy_(hk, non_blocking=True)
-            dv.copy_(hv, non_blocking=True)
-            step(dq, dk, dv)
-            if pg is not None:
-                ellm.memcpy_async(hout.data_ptr(), pg.out(0), d2h, sp)
+            b = j % 2
+            stream.wait_event(ev_up[b])
+            if ev_dl[b] is not None and pg is None:
+                stream.wait_event(ev_dl[b])  # step j-2's result has been read out of outs[b]
+            step(*dev_in[b], o=outs[b])
+            ev_used[b] = torch.cuda.Event()
+            ev_used[b].record(stream)
+            if j + 1 < n_e2e:
+                upload(j + 1)
+            dn.wait_event(ev_used[b])
+            if pg is not None:  # the window is rewritten by the next step: read it on the compute stream
+                ellm.memcpy_async(hout[b].data_ptr(), pg.out(0), d2h, sp)
             else:
-                hout.copy_(out, non_blocking=True)
+                with torch.cuda.stream(dn):
+                    hout[b].copy_(outs[b], non_blocking=True)
+                ev_dl[b] = torch.cuda.Event()
+                ev_dl[b].record(dn)
+        stream.wait_stream(dn)
         e1.record(stream)
         barrier()
         ems = e0.elapsed_time(e1)

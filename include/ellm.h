@@ -368,15 +368,21 @@ int ellm_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
  * cudaMemcpyAsync per maximal contiguous run of the chunk list, one cudaMemcpy2DAsync per maximal
  * evenly strided run), 2 = as 1 for deflate / offload, and a staged inflate: the
  * host link writes 256 MiB batches into a device staging buffer outside the KV pool, then an SM
- * copy moves them into the chunks, 3 = as 1 for deflate / offload, and inflate through a second
- * CUDA context on the pool's device, created by this call: 256 MiB batches host -> a staging
- * buffer allocated by that context -> device-to-device into the chunks, all issued from it on its
- * own stream, ordered against the caller's stream by events (host-link writes into memory of the
- * decode's own context slow a concurrent decode ~2x; into another context's memory ~1.1x:
- * DESIGN.md §5 C3). All are exact byte copies. INVALID_ARG outside 0..3; mode 3 returns CUDA
- * (ellm_last_cuda_error = 10000 + CUresult for a driver failure) or UNSUPPORTED if the side
- * context cannot be created. */
+ * copy moves them into the chunks, 3 = as 1 for deflate / offload, and inflate staged through
+ * memory owned by a second CUDA context on the pool's device (created by this call, once per
+ * pool): 256 MiB batches host -> that context's staging buffer -> device-to-device into the
+ * chunks, all on the caller's stream (host-link writes into memory of the decode's own context
+ * slow a concurrent decode ~2x; into another context's memory ~1.1x: DESIGN.md §5 C3). All are
+ * exact byte copies. INVALID_ARG outside 0..3; mode 3 returns CUDA (ellm_last_cuda_error = 10000 +
+ * CUresult for a driver failure) or UNSUPPORTED if the side context cannot be created. */
 int ellm_set_swap_mode(ellm_pool* pool, int32_t mode);
+/* Host -> device copy of `bytes` from host `src` (pinned) to device `dst` on `stream`, staged in
+ * 256 MiB pieces through the same side-context buffer as swap mode 3 (created on first use), so
+ * that uploading the next step's inputs beside a running decode costs it ~1.1x instead of ~2x
+ * (DESIGN.md §6 e2e). Exact copy; stream-ordered like cudaMemcpyAsync (a use of the staging
+ * buffer on another stream waits for the previous one). INVALID_ARG (null pointer with bytes > 0,
+ * bytes < 0), NO_DEVICE, CUDA / UNSUPPORTED as ellm_set_swap_mode(3). */
+int ellm_upload(ellm_pool* pool, void* dst, const void* src, int64_t bytes, void* stream);
 
 /* ---- introspection (parity tests) --------------------------------------------------- */
 /* table of req: entries[0 .. n_out) for the ceil(len/T) live logical chunks. */

@@ -273,12 +273,12 @@ struct ellm_pool {
   int num_sms = 0;
   ellm::StagingRing ring;
   int swap_mode = 0;                 // 0 SM copy kernel, 1 copy engines, 2 staged inflate, 3 side-context inflate
-  CUcontext side_ctx = nullptr;      // swap_mode 3: second context on the pool's device (copy engines)
-  cudaStream_t side_stream = nullptr;  // ... its stream
-  cudaEvent_t side_before = nullptr;   // recorded on the caller's stream (pool's context)
-  cudaEvent_t side_after = nullptr;    // recorded on side_stream (side context)
-  uint8_t* side_stage = nullptr;       // side context's staging buffer for inflate (256 MiB)
-  int64_t side_stage_chunks = 0;
+  CUcontext side_ctx = nullptr;      // swap mode 3 / ellm_upload: second context on the pool's device
+  uint8_t* side_stage = nullptr;       // ... owning this staging buffer (256 MiB)
+  int64_t side_stage_bytes = 0;
+  cudaEvent_t side_ev = nullptr;       // last use of the staging buffer
+  cudaStream_t side_ev_stream = nullptr;  // ... recorded on this stream
+  bool side_ev_used = false;
   uint8_t* d_stage = nullptr;        // swap_mode 2: device staging buffer for inflate (256 MiB)
   cudaEvent_t stage_ev = nullptr;    // last use of the staging buffer
   cudaStream_t stage_stream = nullptr;

@@ -166,18 +166,17 @@ cudaError_t ce_copy(uint8_t* dst_base, const std::vector<int32_t>& dst, const ui
   return issue_copies(pc, stream);
 }
 
-// Swap mode 3: inflate through a second CUDA context on the pool's device. Measured
-// (tools/interference_ctx2.py, DESIGN.md §5 C3): a concurrent 128 GiB decode step slows 2.33x
-// while host -> device copies land in memory allocated by the decode's own context, 1.67x when
-// another context issues them into that memory, but only 1.08x when they land in memory
-// allocated by the other context — and 1.08x also when that context then moves the data on into
-// the decode's memory with device -> device copies. So inflate copies each batch of up to 256 MiB
-// from the host slots into a staging buffer owned by the side context, then device -> device
-// into the chunks (copy engines, issued from the side context, canonical -> rotated slabs as in
-// ce_copy). Stream order is kept with two events: the side stream waits for the caller's prior
-// work, the caller's stream waits for the copies. The pool VA (VMM, mapped process-wide and
-// granted to the device) and the portable pinned host slots are addressable from the side
-// context. Driver failures are reported as ELLM_ERR_CUDA with last_cuda_error = 10000 + CUresult.
+// Swap mode 3 and ellm_upload: host -> device copies staged through memory owned by a second CUDA
+// context on the pool's device. Measured (tools/interference_ctx2.py, DESIGN.md §5 C3): a
+// concurrent 128 GiB decode step slows 2.33x while host -> device copies land in memory allocated
+// by the decode's own context, 1.67x when another context issues them into that memory, but only
+// 1.06-1.09x when they land in memory allocated by another context — and 1.09-1.11x when the data
+// then moves on into the decode's memory by device -> device copies, issued from either context.
+// So the second context exists only to own a 256 MiB staging buffer; every copy is issued on the
+// caller's stream from the caller's context: host -> staging (copy engine, one copy per run),
+// then staging -> destination (device -> device). The staging buffer is reused in stream order;
+// a use on another stream first waits for the previous use (side_ev). Driver failures creating
+// the context are reported as ELLM_ERR_CUDA with last_cuda_error = 10000 + CUresult.
 constexpr int64_t kSideStageBytes = int64_t(256) << 20;
 void side_destroy(ellm_pool* p);
 int side_init(ellm_pool* p) {
@@ -192,65 +191,61 @@ int side_init(ellm_pool* p) {
     p->last_cuda_error = 10000 + int(r);
     return ELLM_ERR_CUDA;
   }
-  // cuCtxCreate made `c` current: the runtime calls below create its stream, event and buffer
+  // cuCtxCreate made `c` current: the staging buffer is allocated by (owned by) that context
   const int64_t stage = std::max<int64_t>(1, kSideStageBytes / p->chunk_bytes) * p->chunk_bytes;
-  cudaError_t e = cudaStreamCreateWithFlags(&p->side_stream, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->side_after, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&p->side_stage), size_t(stage));
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p->side_stage), size_t(stage));
   d.ctxPopCurrent(&prev);
   p->side_ctx = c;
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->side_before, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->side_ev, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     const int rc = cuda_fail(p, e);
     side_destroy(p);
     return rc;
   }
-  p->side_stage_chunks = stage / p->chunk_bytes;
+  p->side_stage_bytes = stage;
+  p->side_ev_used = false;
   return ELLM_OK;
 }
 void side_destroy(ellm_pool* p) {
   if (!p->side_ctx) return;
   const CtxDriver& d = ctx_driver();
   if (d.ctxPushCurrent(p->side_ctx) == CUDA_SUCCESS) {
-    if (p->side_stream) {
-      cudaStreamSynchronize(p->side_stream);
-      cudaStreamDestroy(p->side_stream);
-    }
-    if (p->side_after) cudaEventDestroy(p->side_after);
     if (p->side_stage) cudaFree(p->side_stage);
     CUcontext prev;
     d.ctxPopCurrent(&prev);
   }
-  if (p->side_before) cudaEventDestroy(p->side_before);
+  if (p->side_ev) cudaEventDestroy(p->side_ev);
   d.ctxDestroy(p->side_ctx);
   p->side_ctx = nullptr;
-  p->side_stream = nullptr;
-  p->side_after = p->side_before = nullptr;
+  p->side_ev = nullptr;
   p->side_stage = nullptr;
 }
-// pool chunks dst[i] <- host slots src[i] through the side context's staging buffer
+// before `stream` reuses the staging buffer: wait for its previous use on another stream
+cudaError_t side_acquire(ellm_pool* p, cudaStream_t stream) {
+  if (p->side_ev_used && p->side_ev_stream != stream) return cudaStreamWaitEvent(stream, p->side_ev, 0);
+  return cudaSuccess;
+}
+cudaError_t side_release(ellm_pool* p, cudaStream_t stream) {
+  p->side_ev_stream = stream;
+  p->side_ev_used = true;
+  return cudaEventRecord(p->side_ev, stream);
+}
+// pool chunks dst[i] <- host slots src[i] through the staging buffer, on `stream`
 cudaError_t side_inflate_copy(ellm_pool* p, uint8_t* pool, const std::vector<int32_t>& dst,
                               const std::vector<int32_t>& src, cudaStream_t stream) {
-  const CtxDriver& d = ctx_driver();
-  cudaError_t e = cudaEventRecord(p->side_before, stream);
-  if (e != cudaSuccess) return e;
-  if (d.ctxPushCurrent(p->side_ctx) != CUDA_SUCCESS) return cudaErrorContextIsDestroyed;
-  e = cudaStreamWaitEvent(p->side_stream, p->side_before, 0);
-  const int64_t S_chunks = p->side_stage_chunks;
+  cudaError_t e = side_acquire(p, stream);
+  const int64_t S_chunks = p->side_stage_bytes / p->chunk_bytes;
   for (size_t b0 = 0; b0 < dst.size() && e == cudaSuccess; b0 += size_t(S_chunks)) {
     const size_t k = std::min(dst.size() - b0, size_t(S_chunks));
     std::vector<int32_t> sidx(k), hs(src.begin() + int64_t(b0), src.begin() + int64_t(b0 + k)),
         ds(dst.begin() + int64_t(b0), dst.begin() + int64_t(b0 + k));
     for (size_t i = 0; i < k; ++i) sidx[i] = int32_t(i);
-    e = ce_copy(p->side_stage, sidx, p->host_slots, hs, p->chunk_bytes, p->side_stream);  // host link
+    e = ce_copy(p->side_stage, sidx, p->host_slots, hs, p->chunk_bytes, stream);  // host link
     if (e == cudaSuccess)  // canonical staging image -> (rotated) chunk slabs
-      e = ce_copy(pool, ds, p->side_stage, sidx, p->chunk_bytes, p->side_stream, p->ash.rot, p->ash.slab, 2);
+      e = ce_copy(pool, ds, p->side_stage, sidx, p->chunk_bytes, stream, p->ash.rot, p->ash.slab, 2);
   }
-  if (e == cudaSuccess) e = cudaEventRecord(p->side_after, p->side_stream);
-  CUcontext prev;
-  d.ctxPopCurrent(&prev);
-  if (e != cudaSuccess) return e;
-  return cudaStreamWaitEvent(stream, p->side_after, 0);
+  if (e == cudaSuccess) e = side_release(p, stream);
+  return e;
 }
 
 // ---- stream-ordered reuse of freed chunks / host slots (see ellm_pool::FreeEvent) ----------
@@ -776,6 +771,25 @@ int ellm_set_swap_mode(ellm_pool* p, int32_t mode) {
   }
   p->swap_mode = mode;
   return ELLM_OK;
+}
+
+int ellm_upload(ellm_pool* p, void* dst, const void* src, int64_t bytes, void* stream) {
+  if (!p || bytes < 0 || (bytes > 0 && (!dst || !src))) return ELLM_ERR_INVALID_ARG;
+  if (!p->has_dev) return ELLM_ERR_NO_DEVICE;
+  if (bytes == 0) return ELLM_OK;
+  if (cudaSetDevice(p->cfg.device) != cudaSuccess) return ELLM_ERR_CUDA;
+  const int rc = side_init(p);
+  if (rc) return rc;
+  cudaStream_t st = S(stream);
+  cudaError_t e = side_acquire(p, st);
+  for (int64_t off = 0; off < bytes && e == cudaSuccess; off += p->side_stage_bytes) {
+    const size_t n = size_t(std::min(p->side_stage_bytes, bytes - off));
+    e = cudaMemcpyAsync(p->side_stage, static_cast<const uint8_t*>(src) + off, n, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(static_cast<uint8_t*>(dst) + off, p->side_stage, n, cudaMemcpyDeviceToDevice, st);
+  }
+  if (e == cudaSuccess) e = side_release(p, st);
+  return e == cudaSuccess ? ELLM_OK : cuda_fail(p, e);
 }
 
 // a2 — O2 in SURVEY §8(c): on-demand chunk mapping at write, all-or-nothing.

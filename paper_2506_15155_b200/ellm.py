@@ -105,6 +105,7 @@ _SIGS = {
     "ellm_set_attn_trace": (ctypes.c_int, [_P, _V, _I32]),
     "ellm_debug_attn_weights": (ctypes.c_int, [_P, _P, _I32]),
     "ellm_memcpy_async": (ctypes.c_int, [_V, _V, _I64, _V]),
+    "ellm_upload": (ctypes.c_int, [_P, _V, _V, _I64, _V]),
     "ellm_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "ellm_last_cuda_error": (ctypes.c_int, [_P]),
     "ellm_kernel_launches": (_I64, [_P]),
@@ -283,6 +284,13 @@ class Pool:
 
     def set_swap_mode(self, mode: int) -> int:
         return ellm_set_swap_mode(self._h, int(mode))
+
+    def upload(self, dst, src, nbytes=None, stream=None) -> int:
+        """host -> device copy staged through the pool's side-context buffer (ellm_upload);
+        dst: device tensor or pointer, src: pinned host tensor or pointer."""
+        if nbytes is None:
+            nbytes = src.numel() * src.element_size()
+        return ellm_upload(self._h, _dptr(dst), _dptr(src), int(nbytes), _sptr(stream))
 
     def set_vmm_overlap(self, premap_bytes: int = 0, async_unmap: bool = False) -> int:
         """f1: speculative pre-mapping budget and asynchronous unmapping."""

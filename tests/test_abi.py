@@ -38,6 +38,8 @@ def test_no_device_pool_refuses_compute():
     assert p.set_swap_mode(4) == ellm.INVALID_ARG and p.set_swap_mode(-1) == ellm.INVALID_ARG
     assert p.set_swap_mode(2) == ellm.OK and p.set_swap_mode(3) == ellm.OK  # no side context without a device
     assert ellm.ellm_set_launch_overlap(p.handle, 2) == ellm.INVALID_ARG
+    assert ellm.ellm_upload(p.handle, 1, 1, -1, None) == ellm.INVALID_ARG
+    assert ellm.ellm_upload(p.handle, 1, 1, 8, None) == ellm.NO_DEVICE
     assert p.set_launch_overlap(True) == ellm.NO_DEVICE
 
 

@@ -98,3 +98,30 @@ def test_side_context_copies_follow_the_callers_stream():
         _check_chunk(pool.read_host_slot(int(slots[i])), wl, 0, i)   # copied out after the appends
         _check_chunk(pool.read_chunk(int(ids[i])), wl, 0, i)          # copied in before the read
     pool.close()
+
+
+def test_upload_through_side_context_is_exact_and_stream_ordered():
+    """ellm_upload stages host -> device copies through the side context's 256 MiB buffer: a
+    300 MiB upload (two pieces) on one stream immediately followed by another upload on a second
+    stream (which must wait for the first one's use of the buffer) lands both byte-exactly, and
+    a kernel queued after the upload on its stream sees the data."""
+    import torch
+    from paper_2506_15155_b200 import ellm
+    pool = ellm.Pool(0, 2, 8, 2, 128, 16, 64, 64, 2, 32, 0)
+    n = 300 << 20
+    g = torch.Generator().manual_seed(5)
+    h1 = torch.randint(0, 256, (n,), dtype=torch.uint8, generator=g).pin_memory()
+    h2 = torch.randint(0, 256, (n // 3,), dtype=torch.uint8, generator=g).pin_memory()
+    d1 = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    d2 = torch.zeros(n // 3, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    assert pool.upload(d1, h1, stream=s1.cuda_stream) == 0, pool.last_cuda_error()
+    assert pool.upload(d2, h2, stream=s2.cuda_stream) == 0
+    with torch.cuda.stream(s1):
+        c1 = d1.sum(dtype=torch.int64)   # queued after the upload on s1
+    torch.cuda.synchronize()
+    assert torch.equal(d1.cpu(), h1) and torch.equal(d2.cpu(), h2)
+    assert int(c1) == int(h1.sum(dtype=torch.int64))
+    assert pool.upload(d1, h1, 0) == 0 and pool.upload(d1, h1, -1) == ellm.INVALID_ARG
+    pool.close()

@@ -80,16 +80,22 @@ def side(kind, ms):
     # ctx2_to_prim = (ctx2, prim), prim_to_ctx2 = (prim, ctx2); ctx2_d2d: ctx2 H2D into its own
     # buffer, then a device -> device copy of it into the primary context's buffer (from ctx2)
     base = kind.replace("_mapped", "")
-    ctx, stream = (prim, s_same) if base in ("same", "prim_to_ctx2", "d2h") else (ctx2, s_2)
+    # prim_to_ctx2_d2d: the primary context copies host -> the second context's buffer, then
+    # device -> device into its own buffer (everything issued from the primary context)
+    ctx, stream = (prim, s_same) if base in ("same", "prim_to_ctx2", "d2h", "prim_to_ctx2_d2d") else (ctx2, s_2)
     dst = d_same if base in ("same", "ctx2_to_prim") else d_2
     ck(cu.cuCtxSetCurrent(ctx))
+    if kind == "ellm_upload":  # the library path: H2D into the side context's staging, then D2D
+        for _ in range(n):
+            assert pool.upload(int(d_same), int(host), N, stream=int(s_same)) == 0
+        return
     hsrc = host_m if kind.endswith("_mapped") else host
     for _ in range(n):
         if kind.startswith("d2h"):  # device -> host from the primary context (a deflate's direction)
             ck(cu.cuMemcpyDtoHAsync(hsrc, d_same, N, stream))
             continue
         ck(cu.cuMemcpyHtoDAsync(dst, hsrc, N, stream))
-        if base == "ctx2_d2d":
+        if base in ("ctx2_d2d", "prim_to_ctx2_d2d"):
             ck(cu.cuMemcpyDtoDAsync(d_same, d_2, N, stream))
     ck(cu.cuCtxSetCurrent(prim))
 
