@@ -20,6 +20,9 @@ def _run(wl, samples, chunk_samples):
     from inputs import gen
     from inputs import workload as W
     from tests.twin import check_attention, torch_to_bits
+    import gc
+    gc.collect()                 # pools of earlier tests in this process (their destructors free
+    torch.cuda.empty_cache()     # the VMM memory) and torch's cached blocks
     free, _ = torch.cuda.mem_get_info()
     need = wl.batch * wl.chunks_per_request * wl.chunk_bytes() + (8 << 30)
     if free < need:

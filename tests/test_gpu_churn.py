@@ -120,6 +120,9 @@ def test_c5_churn_full_size():
     import oracle
     from inputs import gen, workload as W
     from tests.twin import check_attention, torch_to_bits
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()  # earlier tests' pools and torch's cached blocks
     free, _ = torch.cuda.mem_get_info()
     if free < (40 << 30):
         pytest.skip("needs 40 GiB free HBM")

@@ -12,6 +12,9 @@ def _decode_and_check(wl, samples, batch_check=True):
     import oracle
     from inputs import workload as W
     from tests.twin import check_attention, torch_to_bits
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()  # earlier tests' pools and torch's cached blocks
     free, _ = torch.cuda.mem_get_info()
     need = wl.batch * wl.chunks_per_request * wl.chunk_bytes() + (6 << 30)
     if free < need:

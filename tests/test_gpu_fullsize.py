@@ -13,6 +13,9 @@ pytestmark = pytest.mark.gpu
 def c2_pool():
     import torch
     from inputs import workload as W
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()  # earlier tests' pools and torch's cached blocks
     free, _ = torch.cuda.mem_get_info()
     wl = W.c2()
     need = wl.batch * wl.chunks_per_request * wl.chunk_bytes() + (6 << 30)

@@ -18,6 +18,9 @@ def _run(wl, layer, samples):
     from inputs import gen
     from inputs import workload as W
     from tests.twin import bits_to_torch, check_attention, torch_to_bits
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()  # earlier tests' pools and torch's cached blocks
     free, _ = torch.cuda.mem_get_info()
     need = wl.batch * wl.chunks_per_request * wl.chunk_bytes() + (4 << 30)
     if free < need:
