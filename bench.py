@@ -53,6 +53,8 @@ def parse():
                     help="c3: swap-out by layer-wise offload with the commit deferred until the copy "
                          "completed (default), or by deflate (frees the chunks at once, ordered after "
                          "the copy: the decode's next chunk allocation then waits for it)")
+    ap.add_argument("--c3-offload-layers", type=int, default=2,
+                    help="c3: layers of the swap-out enqueued per decode step (offload swap-out)")
     ap.add_argument("--resident", type=int, default=0,
                     help="c3: requests decoding in HBM (0 = as many as fit beside one in flight)")
     ap.add_argument("--gather", choices=["p2p", "nccl"], default="p2p",
@@ -823,6 +825,7 @@ def run_c3(args):
     # the decode's next kv_reserve then takes the lowest free chunk, one of those being copied
     # out, and the compute stream waits for the whole 16 GiB copy-out (stream-ordered reuse, R7).
     pending = None  # (x, ids, slots, e0, em): swap-out copy in flight, commit not yet issued
+    offload_todo = []  # layers of the pending swap-out not yet enqueued
 
     def swap_in_next(x, slots, e0, em):
         nonlocal incoming, in_ev
@@ -842,6 +845,12 @@ def run_c3(args):
 
     def finish_swap_out(block=False):
         nonlocal pending
+        if pending is not None and offload_todo:
+            if not block:
+                offload_some()
+                return
+            while offload_todo:
+                offload_some()
         if pending is None or not (block or pending[4].query()):
             return
         x, ids, slots, e0, em = pending
@@ -877,17 +886,29 @@ def run_c3(args):
         rc, slots = pool.offload_begin(ids)
         if rc:
             raise ellm.EllmError(rc, "c3 offload_begin")
-        for l in range(L):
-            rc = pool.offload_layer(l, ids, sw.cuda_stream)
+        pending = (x, ids, slots, e0, em)
+        offload_todo[:] = list(range(L))
+        offload_some()
+
+    def offload_some():
+        # a few layers per decode step (P:392 layer-wise), not all 16 GiB at once: a step's own
+        # small device -> host copies (read-back of its result) share the copy engines in FIFO
+        # order and would otherwise wait behind the whole copy-out
+        if not offload_todo:
+            return
+        x, ids, slots, e0, em = pending
+        for _ in range(min(args.c3_offload_layers, len(offload_todo))):
+            rc = pool.offload_layer(offload_todo.pop(0), ids, sw.cuda_stream)
             if rc:
                 raise ellm.EllmError(rc, "c3 offload_layer")
-        em.record(sw)                          # swap-out copy done
-        pending = (x, ids, slots, e0, em)
+        if not offload_todo:
+            em.record(sw)                      # swap-out copy done
 
     step_end = []  # per-step end events: the host runs at most LOOKAHEAD steps ahead of the GPU
     LOOKAHEAD = 3
 
-    def step(s, record=False, host=None):
+    def step(s, record=False, host=None, o=None):
+        o = out if o is None else o
         if len(step_end) >= LOOKAHEAD:
             step_end.pop(0).synchronize()
         finish_swap_out()
@@ -904,7 +925,7 @@ def run_c3(args):
             if record:
                 a0 = torch.cuda.Event(enable_timing=True)
                 a0.record(cs)
-            rc = pool.decode_append_attention(l, D, k[l], v[l], q[l], out[l], scale, sp)
+            rc = pool.decode_append_attention(l, D, k[l], v[l], q[l], o[l], scale, sp)
             if rc:
                 raise ellm.EllmError(rc, "c3 decode_append_attention")
             if record:
@@ -977,24 +998,59 @@ def run_c3(args):
     if not args.no_e2e:
         n_e2e = args.swap_every  # one full round, its transition included
         hin = [tuple(x.cpu().pin_memory() for x in inputs[j % NIN]) for j in range(n_e2e)]
-        dev = tuple(torch.empty_like(x) for x in inputs[0])
-        hout = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        # pipelined as in the C2 / C4 e2e: step j+1's inputs copied up on a second stream while
+        # step j runs, step j's output read back on a third; double-buffered
+        dev = [tuple(torch.empty_like(x) for x in inputs[0]) for _ in range(2)]
+        outs = [out, torch.empty_like(out)]
+        hout = [torch.empty(out.shape, dtype=out.dtype).pin_memory() for _ in range(2)]
+        up, dn = torch.cuda.Stream(), torch.cuda.Stream()
+        ev_up, ev_used, ev_dl = [None, None], [None, None], [None, None]
+
+        def upload(j):
+            b = j % 2
+            if ev_used[b] is not None:
+                up.wait_event(ev_used[b])
+            with torch.cuda.stream(up):
+                for dt, ht in zip(dev[b], hin[j]):
+                    dt.copy_(ht, non_blocking=True)
+            ev_up[b] = torch.cuda.Event()
+            ev_up[b].record(up)
+
         s_e = ((s_glob + n_iso) // args.swap_every + 1) * args.swap_every
+        step_ev, host_ms = [], []
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(cs)
+        up.wait_event(e0)
+        upload(0)
         for j in range(n_e2e):
-            for dt, ht in zip(dev, hin[j]):
-                dt.copy_(ht, non_blocking=True)
-            step(s_e + j, host=dev)
-            hout.copy_(out, non_blocking=True)
+            b = j % 2
+            cs.wait_event(ev_up[b])
+            if ev_dl[b] is not None:
+                cs.wait_event(ev_dl[b])
+            t_host = time.perf_counter()
+            step(s_e + j, host=dev[b], o=outs[b])
+            host_ms.append((time.perf_counter() - t_host) * 1e3)
+            ev_used[b] = torch.cuda.Event(enable_timing=True)
+            ev_used[b].record(cs)
+            step_ev.append(ev_used[b])
+            if j + 1 < n_e2e:
+                upload(j + 1)
+            dn.wait_event(ev_used[b])
+            with torch.cuda.stream(dn):
+                hout[b].copy_(outs[b], non_blocking=True)
+            ev_dl[b] = torch.cuda.Event()
+            ev_dl[b].record(dn)
+        cs.wait_stream(dn)
         e1.record(cs)
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
         e2e = {"value": round(R * n_e2e / (ems / 1e3), 3), "unit": UNIT,
                "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() for x in hin[0])),
-               "d2h_bytes_per_step": int(hout.numel() * hout.element_size()),
-               "ms_per_step": round(ems / n_e2e, 3), "steps": n_e2e}
+               "d2h_bytes_per_step": int(hout[0].numel() * hout[0].element_size()),
+               "ms_per_step": round(ems / n_e2e, 3), "steps": n_e2e,
+               "step_end_ms": [round(e0.elapsed_time(x), 1) for x in step_ev],
+               "host_ms_per_step": [round(x, 1) for x in host_ms]}
     torch.cuda.synchronize()
     cpu = None
     if not args.no_cpu_baseline:

@@ -6,6 +6,7 @@
 // Every entry point validates all preconditions before mutating (include/ellm.h
 // "Conventions"); allocation is lowest-id-first (R7).
 #include <algorithm>
+#include <cstdio>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -124,8 +125,14 @@ cudaError_t issue_copies(const std::vector<CopyPiece>& pc, cudaStream_t stream) 
         e = cudaSuccess;
         for (int64_t off = 0; off < total && e == cudaSuccess; off += step)
           e = cudaMemcpyAsync(a.d + off, a.s + off, size_t(std::min(step, total - off)), cudaMemcpyDefault, stream);
-      } else
-        e = cudaMemcpy2DAsync(a.d, size_t(dp), a.s, size_t(sp), size_t(a.n), rows, cudaMemcpyDefault, stream);
+      } else {
+        // strided run: rows of a.n bytes, split into groups of at most `cap` bytes as well
+        const size_t step = cap > 0 ? std::max<size_t>(1, size_t(cap / a.n)) : rows;
+        e = cudaSuccess;
+        for (size_t r0 = 0; r0 < rows && e == cudaSuccess; r0 += step)
+          e = cudaMemcpy2DAsync(a.d + int64_t(r0) * dp, size_t(dp), a.s + int64_t(r0) * sp, size_t(sp), size_t(a.n),
+                                std::min(step, rows - r0), cudaMemcpyDefault, stream);
+      }
       if (e != cudaSuccess) return e;
     } else {
       cudaError_t e = cudaMemcpyAsync(a.d, a.s, size_t(a.n), cudaMemcpyDefault, stream);
@@ -281,7 +288,14 @@ cudaError_t wait_freed(ellm_pool* p, std::vector<int32_t>& tag, int64_t id, cuda
   const int32_t i = tag[size_t(id)];
   if (i < 0) return cudaSuccess;
   cudaError_t e = cudaSuccess;
-  if (p->free_events[size_t(i)].stream != stream) e = cudaStreamWaitEvent(stream, p->free_events[size_t(i)].ev, 0);
+  if (p->free_events[size_t(i)].stream != stream) {
+    static const bool dbg = std::getenv("ELLM_DEBUG_WAITS") != nullptr;  // measurement aid
+    if (dbg && cudaEventQuery(p->free_events[size_t(i)].ev) == cudaErrorNotReady)
+      std::fprintf(stderr, "[ellm] stream %p waits for unfinished work on stream %p (%s %lld)\n",
+                   static_cast<void*>(stream), static_cast<void*>(p->free_events[size_t(i)].stream),
+                   &tag == &p->chunk_ev ? "chunk" : "slot", static_cast<long long>(id));
+    e = cudaStreamWaitEvent(stream, p->free_events[size_t(i)].ev, 0);
+  }
   tag[size_t(id)] = -1;
   drop_ref(p, i);
   return e;

@@ -4,6 +4,8 @@
 #include <time.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -116,6 +118,9 @@ int StagingRing::retire_and_advance() {
   if (int rc = flush_pending(cur_)) return rc;
   Seg& s = segs_[size_t(cur_)];
   for (auto e : s.events) {  // the segment's previous consumers must be done
+    static const bool dbg = std::getenv("ELLM_DEBUG_WAITS") != nullptr;  // measurement aid
+    if (dbg && cudaEventQuery(e) == cudaErrorNotReady)
+      std::fprintf(stderr, "[ellm] staging ring: host waits for segment %d's consumers\n", cur_);
     if (cudaEventSynchronize(e) != cudaSuccess) return ELLM_ERR_CUDA;
     free_events_.push_back(e);
   }
