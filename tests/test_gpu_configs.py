@@ -58,11 +58,13 @@ def test_c2_kv_head_shard(world, rank):
     _decode_and_check(W.c2(world, rank), [(5, 31), (30, 2)])
 
 
-def test_c3_128k_contexts_with_swap_under_pressure():
+@pytest.mark.parametrize("mode", [0, 3])
+def test_c3_128k_contexts_with_swap_under_pressure(mode):
     """8B-262K shape, 4 requests x 131072 tokens (64 GiB of KV) in a device pool that holds
     3 of them: request 3 is prefilled, swapped out (deflate) to make room, request 0 is
     swapped out, request 3 swapped back in (inflate into request 0's freed chunks), then
-    decode attention of the resident set is checked against the oracle."""
+    decode attention of the resident set is checked against the oracle. mode 0: SM copy
+    kernels; mode 3: copy engines, the 16 GiB inflate staged through the side context."""
     import torch
     import oracle
     from inputs import workload as W
@@ -73,6 +75,7 @@ def test_c3_128k_contexts_with_swap_under_pressure():
     cpr = wl.chunks_per_request  # 8193
     pool = ellm.Pool(0, 32, 32, 8, 128, 16, 4 * cpr, 3 * cpr + 1, 4, cpr, cpr)
     try:
+        assert pool.set_swap_mode(mode) == 0
         s = torch.cuda.current_stream().cuda_stream
         # prefill requests 0..2, then free room for request 3 by deflating request 2's chunks
         sub = W.Workload(**{**wl.__dict__, "batch": 3})
